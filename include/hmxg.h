@@ -1,0 +1,132 @@
+/*
+ * hmxg.h — C-ABI of the B200 HMatrix x W evaluator (libhmxg.so).
+ *
+ * Drop-in boundary for the reference's evaluation phase
+ *   hmx::evaluate(const CDS&, const EvalPlan&, const DenseMatrix& w, [WorkerPool&,] EvalStats*)
+ *   (/root/reference/proj/include/hmx/executor.hpp:51-54,
+ *    /root/reference/proj/src/executor.cpp:274-302).
+ * The caller keeps building the tree / interactions / compression / CDS on the host
+ * (reference inspector, or this repo's instance builder) and hands the CDS over as a
+ * POD view of raw arrays; nothing here knows about torch or C++ types.
+ *
+ * Status codes: 0 ok, 1 invalid argument, 2 CUDA error, 3 out of memory,
+ * 4 NCCL/collective error. A thread-local message is kept for hmxg_last_error().
+ */
+#ifndef HMXG_H_
+#define HMXG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMXG_OK 0
+#define HMXG_EINVAL 1
+#define HMXG_ECUDA 2
+#define HMXG_ENOMEM 3
+#define HMXG_ECOMM 4
+
+#define HMXG_NO_NODE 0xffffffffu
+
+/* hmxg_evaluate flags */
+#define HMXG_F_DEVICE_PTRS 0x1u /* W and Y are device pointers on the matrix's (single) device */
+#define HMXG_F_NO_SYNC 0x2u     /* with DEVICE_PTRS: enqueue on `stream` and return */
+
+/*
+ * View of a computation-ordered CDS (reference struct hmx::CDS,
+ * /root/reference/proj/include/hmx/structure.hpp:83-130). All arrays are borrowed for
+ * the duration of hmxg_upload only.
+ *   tree arrays            : num_nodes entries (ClusterTree, tree.hpp:19-33), kNoNode = HMXG_NO_NODE
+ *   perm                   : n entries, node i owns perm[start[i], end[i])
+ *   near_pairs / far_pairs : 2*num_near / 2*num_far (i,j) in storage order
+ *                            (= BlockSet::flat_pairs(), structure.cpp:21-27)
+ *   v_order                : num_v node ids in V storage order (coarsenset traversal,
+ *                            structure.cpp:197-202)
+ *   dptr / bptr / vptr     : num_near+1 / num_far+1 / num_v+1 element offsets
+ *   dgen / bgen / vgen     : FP64 generators, column major: D_ij m_i x m_j, B_ij sr_i x sr_j,
+ *                            V_i v_width(i) x sr_i (v_width = leaf size or sr_lc + sr_rc).
+ */
+typedef struct hmxg_cds_view {
+  uint64_t n;
+  uint32_t num_nodes;
+  uint32_t height;
+  const uint32_t* parent;
+  const uint32_t* lchild;
+  const uint32_t* rchild;
+  const uint32_t* start;
+  const uint32_t* end;
+  const uint32_t* level;
+  const uint32_t* perm;
+  const uint32_t* sranks;
+  const uint8_t* participating;
+  uint64_t num_near;
+  const uint32_t* near_pairs;
+  uint64_t num_far;
+  const uint32_t* far_pairs;
+  uint64_t num_v;
+  const uint32_t* v_order;
+  const uint64_t* dptr;
+  const uint64_t* bptr;
+  const uint64_t* vptr;
+  const double* dgen;
+  const double* bgen;
+  const double* vgen;
+} hmxg_cds_view;
+
+/* EvalStats (executor.hpp:43-46) plus device-side accounting. */
+typedef struct hmxg_stats {
+  uint64_t locked_pairs; /* always 0: every output tile has one writer */
+  double seconds;        /* host wall time of the call (reference semantics) */
+  double device_ms;      /* device time of the evaluation launches (max over devices) */
+  uint32_t launches;     /* kernel launches issued by this call (all devices) */
+} hmxg_stats;
+
+/* Static description of an uploaded matrix (roofline accounting). */
+typedef struct hmxg_info {
+  uint64_t n;
+  uint64_t d_elems, b_elems, v_elems; /* |Dgen|, |Bgen|, |Vgen| */
+  uint64_t skel_rows;                 /* sum of active sranks (T/S rows) */
+  uint32_t num_devices;
+  uint32_t launches_per_eval;         /* kernels per evaluate call per device */
+  double flops_per_col;               /* 2*(2|V|+|B|+|D|) */
+  uint64_t device_bytes;              /* resident generator + table bytes per device */
+} hmxg_info;
+
+typedef struct hmxg_ctx hmxg_ctx;
+typedef struct hmxg_mat hmxg_mat;
+
+/* Context over `ndev` CUDA devices (devs may repeat a device id: each entry is one
+ * column shard). ndev = 0 / devs = NULL means {0}. */
+int hmxg_create(const int* devs, int ndev, hmxg_ctx** out);
+int hmxg_destroy(hmxg_ctx* ctx);
+
+/* Validate the view, derive the level-batched task tables and copy the generators to
+ * every device of the context (replicated CDS). */
+int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out);
+int hmxg_free(hmxg_mat* mat);
+/* Host-only check of a view (no device needed): the structural invariants hmxg_upload
+ * enforces. Returns HMXG_OK or HMXG_EINVAL with the reason in hmxg_last_error(). On
+ * success, if info != NULL, the size fields (n, *_elems, skel_rows, launches_per_eval,
+ * flops_per_col) are filled. */
+int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info);
+int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info);
+
+/* Y = K~ W. W is n x q column major with leading dimension ldw >= n, Y likewise.
+ * Host pointers (default): columns are sharded over the context's devices, copied in,
+ * evaluated and copied back; returns when Y is complete.
+ * HMXG_F_DEVICE_PTRS: W/Y live on the matrix's device (single-device contexts only);
+ * `stream` (cudaStream_t, may be NULL = internal stream) orders the work.
+ * q == 0 is a no-op (Y is n x 0); a row mismatch (n != cds.n) is HMXG_EINVAL. */
+int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y,
+                  size_t ldy, unsigned flags, void* stream, hmxg_stats* stats);
+
+const char* hmxg_last_error(void);
+const char* hmxg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMXG_H_ */

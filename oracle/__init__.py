@@ -1,0 +1,234 @@
+"""Parity oracle for the B200 evaluator — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference``
+legs import this package, and only to check or time against it; the product package
+(paper_1812_07152_b200/) never imports, links or loads anything from here.
+
+Two checkers:
+* ``build/libhmxo.so`` — hmx_oracle.c, a C restatement of the reference evaluation
+  (/root/reference/proj/src/executor.cpp:23-302, dense.cpp:13-66) that reproduces the
+  reference's bits (pinned in tests/test_oracle.py).
+* ``_ref/libhmx_ref.so`` — the unmodified reference library compiled from
+  /root/reference/proj/src by oracle/Makefile, driven through ref_capi.cpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+from paper_1812_07152_b200 import _native as N
+from paper_1812_07152_b200.cds import CDS
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "build", "libhmxo.so")
+REF_SO = os.path.join(HERE, "_ref", "libhmx_ref.so")
+
+_libs: dict = {}
+
+
+def _oracle_lib():
+    if "o" not in _libs:
+        lib = C.CDLL(ORACLE_SO)
+        lib.hmxo_evaluate.restype = C.c_int
+        lib.hmxo_evaluate.argtypes = [C.POINTER(N.CdsView), C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                      C.c_void_p, C.c_size_t]
+        lib.hmxo_flops_per_col.restype = C.c_double
+        lib.hmxo_flops_per_col.argtypes = [C.POINTER(N.CdsView)]
+        _libs["o"] = lib
+    return _libs["o"]
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def _ref_lib():
+    if "r" not in _libs:
+        lib = C.CDLL(REF_SO)
+        vp, u64, f64p = C.c_void_p, C.c_uint64, C.POINTER(C.c_double)
+        sig = {
+            "hmxr_spec_default": (None, [C.POINTER(RefSpec)]),
+            "hmxr_instance_new": (C.c_int, [C.POINTER(RefSpec), C.POINTER(vp)]),
+            "hmxr_instance_free": (None, [vp]),
+            "hmxr_instance_view": (C.c_int, [vp, C.POINTER(N.CdsView)]),
+            "hmxr_points": (C.c_int, [vp, C.POINTER(f64p), C.POINTER(u64), C.POINTER(u64)]),
+            "hmxr_random_matrix": (C.c_int, [u64, u64, u64, vp]),
+            "hmxr_evaluate": (C.c_int, [vp, vp, u64, u64, vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+            "hmxr_evaluate_ref": (C.c_int, [vp, vp, u64, u64, vp]),
+            "hmxr_dense_apply": (C.c_int, [vp, vp, u64, u64, vp]),
+            "hmxr_relative_error_dense": (C.c_int, [vp, vp, u64, u64, C.POINTER(C.c_double)]),
+            "hmxr_cds_from_view": (C.c_int, [C.POINTER(N.CdsView), C.POINTER(vp)]),
+            "hmxr_cds_free": (None, [vp]),
+            "hmxr_cds_evaluate": (C.c_int, [vp, vp, u64, u64, vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+            "hmxr_last_error": (C.c_char_p, []),
+            "hmxr_hardware_workers": (C.c_uint, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        _libs["r"] = lib
+    return _libs["r"]
+
+
+def _ref_check(rc: int) -> None:
+    if rc:
+        msg = _ref_lib().hmxr_last_error().decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(f"reference status {rc}: {msg}")
+
+
+def oracle_evaluate(cds: CDS, w: np.ndarray) -> np.ndarray:
+    """Y = K~ W by the C restatement (p = 1 semantics of hmx::evaluate)."""
+    wf = np.asfortranarray(w, dtype=np.float64)
+    n, q = wf.shape
+    y = np.zeros((n, q), dtype=np.float64, order="F")
+    v = cds.view()
+    rc = _oracle_lib().hmxo_evaluate(C.byref(v), wf.ctypes.data_as(C.c_void_p), n, q, n,
+                                     y.ctypes.data_as(C.c_void_p), n)
+    if rc == 1:
+        raise ValueError("evaluate: W row count does not match the point count")
+    if rc:
+        raise RuntimeError(f"oracle status {rc}")
+    return y
+
+
+class RefSpec(C.Structure):
+    """``hmxr_spec`` — tst::InstanceSpec (proj/tests/helpers.hpp:81-99)."""
+
+    _fields_ = [
+        ("n", C.c_uint64), ("d", C.c_uint64), ("shape", C.c_int32), ("mode", C.c_int32), ("tau", C.c_double),
+        ("leaf", C.c_uint32), ("kernel", C.c_int32), ("h", C.c_double), ("bacc", C.c_double),
+        ("max_rank", C.c_uint32), ("sample_exact", C.c_int32), ("budget", C.c_uint32), ("knn_k", C.c_uint32),
+        ("p", C.c_uint32), ("agg", C.c_uint32), ("near_bs", C.c_uint32), ("far_bs", C.c_uint32),
+        ("seed", C.c_uint64),
+    ]
+
+
+@dataclass
+class RefInstanceSpec:
+    """Python face of tst::InstanceSpec; shape 0 grid2d / 1 uniform / 2 sphere, mode 0 tau / 1 hss."""
+
+    n: int = 512
+    d: int = 2
+    shape: int = 1
+    mode: int = 1
+    tau: float = 0.0
+    leaf: int = 64
+    kernel: int = 0
+    h: float = 1.0
+    bacc: float = 1e-5
+    max_rank: int = 64
+    sample_exact: int = 0
+    budget: int = 128
+    knn_k: int = 16
+    p: int = 4
+    agg: int = 2
+    near_bs: int = 2
+    far_bs: int = 4
+    seed: int = 1
+
+
+class RefInstance:
+    """``tst::make_instance`` run by the reference library; ``cds`` is its own CDS."""
+
+    def __init__(self, spec: RefInstanceSpec):
+        lib = _ref_lib()
+        s = RefSpec()
+        for f in fields(spec):
+            setattr(s, f.name, getattr(spec, f.name))
+        h = C.c_void_p()
+        _ref_check(lib.hmxr_instance_new(C.byref(s), C.byref(h)))
+        self._h = h
+        self.spec = spec
+        v = N.CdsView()
+        lib.hmxr_instance_view(h, C.byref(v))
+        self.cds = CDS.from_view(v, owner=self)
+
+    def evaluate(self, w: np.ndarray, plan_bits: int = 0, p: int = 1) -> np.ndarray:
+        wf = np.asfortranarray(w, dtype=np.float64)
+        y = np.zeros(wf.shape, dtype=np.float64, order="F")
+        sec = C.c_double()
+        _ref_check(_ref_lib().hmxr_evaluate(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1],
+                                            y.ctypes.data_as(C.c_void_p), plan_bits, p, C.byref(sec)))
+        return y
+
+    def evaluate_reference(self, w: np.ndarray) -> np.ndarray:
+        wf = np.asfortranarray(w, dtype=np.float64)
+        y = np.zeros(wf.shape, dtype=np.float64, order="F")
+        _ref_check(_ref_lib().hmxr_evaluate_ref(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1],
+                                                y.ctypes.data_as(C.c_void_p)))
+        return y
+
+    def dense_apply(self, w: np.ndarray) -> np.ndarray:
+        wf = np.asfortranarray(w, dtype=np.float64)
+        y = np.zeros(wf.shape, dtype=np.float64, order="F")
+        _ref_check(_ref_lib().hmxr_dense_apply(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1],
+                                               y.ctypes.data_as(C.c_void_p)))
+        return y
+
+    def relative_error_dense(self, w: np.ndarray) -> float:
+        wf = np.asfortranarray(w, dtype=np.float64)
+        eps = C.c_double()
+        _ref_check(_ref_lib().hmxr_relative_error_dense(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0],
+                                                        wf.shape[1], C.byref(eps)))
+        return eps.value
+
+    def close(self):
+        if self._h:
+            self.cds._cache.clear()
+            _ref_lib().hmxr_instance_free(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RefCds:
+    """The reference ``evaluate`` over any CDS (rebuilt as an hmx::CDS from the view)."""
+
+    def __init__(self, cds: CDS):
+        h = C.c_void_p()
+        v = cds.view()
+        _ref_check(_ref_lib().hmxr_cds_from_view(C.byref(v), C.byref(h)))
+        self._h = h
+        self.n = cds.n
+
+    def evaluate(self, w: np.ndarray, p: int = 1, plan_bits: int = 0) -> tuple[np.ndarray, float]:
+        wf = np.asfortranarray(w, dtype=np.float64)
+        y = np.zeros(wf.shape, dtype=np.float64, order="F")
+        sec = C.c_double()
+        _ref_check(_ref_lib().hmxr_cds_evaluate(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1],
+                                                y.ctypes.data_as(C.c_void_p), plan_bits, p, C.byref(sec)))
+        return y, sec.value
+
+    def close(self):
+        if self._h:
+            _ref_lib().hmxr_cds_free(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def random_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """tst::random_matrix (helpers.hpp:53-58): uniform[-1, 1) via the reference Rng."""
+    out = np.zeros((rows, cols), dtype=np.float64, order="F")
+    _ref_lib().hmxr_random_matrix(rows, cols, seed, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def rel_frob(a: np.ndarray, b: np.ndarray) -> float:
+    """helpers.hpp:60-68."""
+    num = float(np.sum((np.asarray(a) - np.asarray(b)) ** 2))
+    den = float(np.sum(np.asarray(b) ** 2))
+    return float(np.sqrt(num)) if den == 0.0 else float(np.sqrt(num / den))

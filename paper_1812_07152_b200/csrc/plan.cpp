@@ -1,0 +1,238 @@
+// plan.cpp — CDS validation and lowering to level-batched task tables (see plan.hpp).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <limits>
+#include <sstream>
+
+namespace hmxg {
+
+namespace {
+
+constexpr std::uint64_t kNoSlot = std::numeric_limits<std::uint64_t>::max();
+
+template <class... A>
+bool fail(std::string& err, A&&... parts) {
+  std::ostringstream os;
+  (os << ... << parts);
+  err = os.str();
+  return false;
+}
+
+}  // namespace
+
+bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err) {
+  plan = Plan{};
+  const std::uint32_t nn = v.num_nodes;
+  if (nn == 0) return fail(err, "cds: empty tree");
+  if (!v.parent || !v.lchild || !v.rchild || !v.start || !v.end || !v.level || !v.perm ||
+      !v.sranks || !v.participating || !v.dptr || !v.bptr || !v.vptr)
+    return fail(err, "cds: null array in view");
+  if ((v.num_near && (!v.near_pairs || !v.dgen)) || (v.num_far && (!v.far_pairs || !v.bgen)) ||
+      (v.num_v && (!v.v_order || !v.vgen)))
+    return fail(err, "cds: null pair list or generator array in view");
+  if (v.n == 0 || v.n > std::numeric_limits<std::uint32_t>::max())
+    return fail(err, "cds: point count out of range");
+  if (v.parent[0] != HMXG_NO_NODE || v.start[0] != 0 || v.end[0] != v.n)
+    return fail(err, "cds: node 0 must be the root covering [0, n)");
+  plan.n = v.n;
+  plan.num_nodes = nn;
+
+  // --- tree structure (ClusterTree invariants, proj/src/tree.cpp:27-47)
+  std::vector<std::uint8_t> seen(v.n, 0);
+  for (std::uint64_t p = 0; p < v.n; ++p) {
+    if (v.perm[p] >= v.n || seen[v.perm[p]]) return fail(err, "cds: perm is not a bijection");
+    seen[v.perm[p]] = 1;
+  }
+  auto is_leaf = [&](std::uint32_t i) { return v.lchild[i] == HMXG_NO_NODE; };
+  std::vector<std::uint32_t> order;  // BFS from the root
+  order.reserve(nn);
+  order.push_back(0);
+  for (std::size_t qi = 0; qi < order.size(); ++qi) {
+    const std::uint32_t i = order[qi];
+    if (v.start[i] > v.end[i] || v.end[i] > v.n) return fail(err, "cds: bad range of node ", i);
+    if (is_leaf(i)) {
+      if (v.rchild[i] != HMXG_NO_NODE) return fail(err, "cds: half-leaf node ", i);
+      continue;
+    }
+    const std::uint32_t l = v.lchild[i], r = v.rchild[i];
+    if (l >= nn || r >= nn || l == r) return fail(err, "cds: bad children of node ", i);
+    if (v.parent[l] != i || v.parent[r] != i) return fail(err, "cds: bad parent link under ", i);
+    if (v.start[l] != v.start[i] || v.end[l] != v.start[r] || v.end[r] != v.end[i])
+      return fail(err, "cds: children do not partition node ", i);
+    if (v.level[l] != v.level[i] + 1 || v.level[r] != v.level[i] + 1)
+      return fail(err, "cds: level of children of node ", i);
+    order.push_back(l);
+    order.push_back(r);
+    if (order.size() > nn) return fail(err, "cds: tree has a cycle");
+  }
+  if (order.size() != nn) return fail(err, "cds: nodes unreachable from the root");
+  std::uint32_t height = 0;
+  for (std::uint32_t i = 0; i < nn; ++i) height = std::max(height, v.level[i]);
+  std::vector<std::uint32_t> sub_h(nn, 0);  // longest downward path (tree.cpp:19-25)
+  for (std::size_t qi = order.size(); qi-- > 0;) {
+    const std::uint32_t i = order[qi];
+    if (!is_leaf(i)) sub_h[i] = 1 + std::max(sub_h[v.lchild[i]], sub_h[v.rchild[i]]);
+  }
+
+  auto active = [&](std::uint32_t i) { return v.participating[i] && v.sranks[i] > 0; };
+  auto size_of = [&](std::uint32_t i) { return v.end[i] - v.start[i]; };
+  auto v_width = [&](std::uint32_t i) -> std::uint64_t {
+    return is_leaf(i) ? size_of(i) : std::uint64_t(v.sranks[v.lchild[i]]) + v.sranks[v.rchild[i]];
+  };
+  for (std::uint32_t i = 0; i < nn; ++i) {
+    if (!active(i) || is_leaf(i)) continue;
+    // participation is closed downward (proj/src/interaction.cpp:145-157)
+    if (!v.participating[v.lchild[i]] || !v.participating[v.rchild[i]])
+      return fail(err, "cds: active node ", i, " has a non-participating child");
+  }
+
+  // --- generator slots and sizes (structure.hpp:88-130)
+  std::vector<std::uint64_t> vslot(nn, kNoSlot);
+  for (std::uint64_t s = 0; s < v.num_v; ++s) {
+    const std::uint32_t i = v.v_order[s];
+    if (i >= nn || vslot[i] != kNoSlot) return fail(err, "cds: bad v_order entry ", s);
+    vslot[i] = s;
+    if (v.vptr[s + 1] < v.vptr[s] || v.vptr[s + 1] - v.vptr[s] != v_width(i) * v.sranks[i])
+      return fail(err, "cds: V generator of node ", i, " has the wrong size");
+  }
+  for (std::uint32_t i = 0; i < nn; ++i)
+    if (active(i) && vslot[i] == kNoSlot) return fail(err, "cds: node ", i, " has no basis generator");
+  std::vector<std::vector<std::uint64_t>> far_of(nn), near_of(nn);
+  for (std::uint64_t s = 0; s < v.num_far; ++s) {
+    const std::uint32_t i = v.far_pairs[2 * s], j = v.far_pairs[2 * s + 1];
+    if (i >= nn || j >= nn) return fail(err, "cds: far pair ", s, " out of range");
+    if (v.bptr[s + 1] < v.bptr[s] ||
+        v.bptr[s + 1] - v.bptr[s] != std::uint64_t(v.sranks[i]) * v.sranks[j])
+      return fail(err, "cds: far generator ", s, " has the wrong size");
+    if (v.sranks[i] == 0 || v.sranks[j] == 0) continue;  // no-op pair, executor.cpp:107
+    if (!active(i) || !active(j)) return fail(err, "cds: far pair ", s, " touches a non-participating node");
+    far_of[i].push_back(s);
+  }
+  for (std::uint64_t s = 0; s < v.num_near; ++s) {
+    const std::uint32_t i = v.near_pairs[2 * s], j = v.near_pairs[2 * s + 1];
+    if (i >= nn || j >= nn || !is_leaf(i) || !is_leaf(j)) return fail(err, "cds: near pair ", s, " is not a leaf pair");
+    if (v.dptr[s + 1] < v.dptr[s] ||
+        v.dptr[s + 1] - v.dptr[s] != std::uint64_t(size_of(i)) * size_of(j))
+      return fail(err, "cds: near generator ", s, " has the wrong size");
+    near_of[i].push_back(s);
+  }
+  plan.d_elems = v.dptr[v.num_near];
+  plan.b_elems = v.bptr[v.num_far];
+  plan.v_elems = v.vptr[v.num_v];
+  if (std::max({plan.d_elems, plan.b_elems, plan.v_elems}) >= (std::uint64_t(1) << 62))
+    return fail(err, "cds: generator arrays too large");
+
+  // --- T/S rows: siblings adjacent so [T_lc; T_rc] is one contiguous operand
+  plan.node_off.assign(nn, 0);
+  std::uint64_t rows = 0;
+  if (active(0)) {
+    plan.node_off[0] = rows;
+    rows += v.sranks[0];
+  }
+  for (std::uint32_t i : order) {
+    if (is_leaf(i)) continue;
+    for (std::uint32_t c : {v.lchild[i], v.rchild[i]}) {
+      plan.node_off[c] = rows;
+      if (active(c)) rows += v.sranks[c];
+    }
+  }
+  if (rows > std::numeric_limits<std::uint32_t>::max()) return fail(err, "cds: too many skeleton rows");
+  plan.skel_rows = rows;
+
+  const std::uint32_t bm = tile_m;
+  auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs,
+                       double& phase_flops) {
+    const std::uint32_t tiles = m == 0 ? 0 : (m + bm - 1) / bm;
+    for (std::uint32_t t = 0; t < tiles; ++t) {
+      const std::uint32_t r0 = t * bm;
+      Task task{};
+      task.c_row = static_cast<std::uint32_t>(c_row + r0);
+      task.cbuf = cbuf;
+      task.m = static_cast<std::uint16_t>(std::min(bm, m - r0));
+      task.seg_begin = static_cast<std::uint32_t>(plan.segs.size());
+      emit_segs(r0);
+      task.seg_end = static_cast<std::uint32_t>(plan.segs.size());
+      for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s)
+        phase_flops += 2.0 * task.m * plan.segs[s].k;
+      plan.tasks.push_back(task);
+    }
+    plan.max_m = std::max(plan.max_m, m);
+  };
+  auto push_seg = [&](Gen gen, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k, Buf bbuf,
+                      std::uint64_t b_row) {
+    if (k == 0) return;
+    plan.segs.push_back(Seg{a_off, static_cast<std::uint32_t>(lda), static_cast<std::uint32_t>(k),
+                            static_cast<std::uint32_t>(b_row), static_cast<std::uint16_t>(gen),
+                            static_cast<std::uint16_t>(bbuf)});
+  };
+  auto open_phase = [&](PhaseKind kind, bool trans, std::uint32_t level) {
+    plan.phases.push_back(Phase{kind, trans, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0});
+  };
+  auto close_phase = [&]() {
+    Phase& ph = plan.phases.back();
+    ph.task_end = static_cast<std::uint32_t>(plan.tasks.size());
+    if (ph.task_end == ph.task_begin) plan.phases.pop_back();
+  };
+
+  // --- upward, by subtree height: T_i = V_i^T * (leaf ? Wp_i : [T_lc; T_rc])
+  std::uint32_t max_h = 0;
+  for (std::uint32_t i = 0; i < nn; ++i) max_h = std::max(max_h, sub_h[i]);
+  for (std::uint32_t h = 0; h <= max_h; ++h) {
+    open_phase(kPhaseUp, true, h);
+    for (std::uint32_t i : order) {
+      if (sub_h[i] != h || !active(i)) continue;
+      const std::uint64_t lda = v_width(i);
+      const std::uint64_t vo = v.vptr[vslot[i]];
+      add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0) {
+        if (is_leaf(i))
+          push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufWp, v.start[i]);
+        else
+          push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufT, plan.node_off[v.lchild[i]]);
+      }, plan.phases.back().flops_per_col);
+    }
+    close_phase();
+  }
+
+  // --- downward with the far pass folded in, by depth:
+  //     S_c = sum_{far (c,j)} B_cj T_j + V_p[rows of c] S_p
+  for (std::uint32_t d = 0; d <= height; ++d) {
+    open_phase(kPhaseDown, false, d);
+    for (std::uint32_t c : order) {
+      if (v.level[c] != d || !active(c)) continue;
+      const std::uint32_t p = v.parent[c];
+      add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0) {
+        for (std::uint64_t s : far_of[c]) {
+          const std::uint32_t j = v.far_pairs[2 * s + 1];
+          push_seg(kGenB, v.bptr[s] + r0, v.sranks[c], v.sranks[j], kBufT, plan.node_off[j]);
+        }
+        if (p != HMXG_NO_NODE && active(p)) {
+          const std::uint64_t row_in_parent = (c == v.lchild[p]) ? 0 : v.sranks[v.lchild[p]];
+          push_seg(kGenV, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], kBufS,
+                   plan.node_off[p]);
+        }
+      }, plan.phases.back().flops_per_col);
+    }
+    close_phase();
+  }
+
+  // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j (every leaf row written once)
+  open_phase(kPhaseLeaf, false, 0);
+  for (std::uint32_t i : order) {
+    if (!is_leaf(i)) continue;
+    const std::uint32_t m = size_of(i);
+    add_tiles(m, kBufYp, v.start[i], [&](std::uint32_t r0) {
+      if (active(i)) push_seg(kGenV, v.vptr[vslot[i]] + r0, m, v.sranks[i], kBufS, plan.node_off[i]);
+      for (std::uint64_t s : near_of[i]) {
+        const std::uint32_t j = v.near_pairs[2 * s + 1];
+        push_seg(kGenD, v.dptr[s] + r0, m, size_of(j), kBufWp, v.start[j]);
+      }
+    }, plan.phases.back().flops_per_col);
+  }
+  close_phase();
+  if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())
+    return fail(err, "cds: too many GEMM segments");
+  return true;
+}
+
+}  // namespace hmxg

@@ -1,0 +1,223 @@
+"""Python mirror of the reference executor API over the B200 C-ABI.
+
+Reference: /root/reference/proj/include/hmx/executor.hpp:18-81 and
+proj/src/executor.cpp:259-302.
+
+* ``EvalPlan`` / ``PlanDefaults`` / ``generate_plan`` keep the reference's lowering
+  switches. The switches only pick a CPU schedule, and every schedule gives the same
+  result. The B200 evaluator accepts a plan and runs its own level-batched schedule
+  (``plan_pseudocode`` prints it).
+* ``evaluate(cds, plan, w, stats=None)`` has the same semantics as ``hmx::evaluate``.
+  A W row count that does not match raises ``ValueError`` (std::invalid_argument,
+  executor.cpp:277-278). Q == 0 returns an n x 0 result (:279-282). ``stats`` gets
+  ``locked_pairs == 0`` and the wall ``seconds``.
+* ``Evaluator`` is the explicit handle: a context over one or more devices plus the
+  uploaded matrix. Columns are sharded over the devices.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .cds import CDS
+
+
+class HmxgError(RuntimeError):
+    """A non-argument failure of the native evaluator (CUDA, memory, collective)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[hmxg status {code}] {msg}")
+        self.code = code
+
+
+def _check(rc: int) -> None:
+    if rc == N.HMXG_OK:
+        return
+    msg = N.last_error(N.hmxg(), "hmxg")
+    if rc == N.HMXG_EINVAL:
+        raise ValueError(msg)
+    raise HmxgError(rc, msg)
+
+
+@dataclass
+class EvalPlan:
+    """Lowering switches (executor.hpp:20-28); results-invariant by construction."""
+
+    block_lowering_near: bool = False
+    block_lowering_far: bool = False
+    coarsen_lowering: bool = False
+    peel_top: bool = False
+    p: int = 1
+    block_threshold: int = 0
+    coarsen_threshold: int = 4
+
+
+@dataclass
+class PlanDefaults:
+    block_threshold: int = 0
+    coarsen_threshold: int = 4
+    p: int = 0
+
+
+@dataclass
+class EvalStats:
+    """executor.hpp:43-46 plus the device-side accounting of the B200 run."""
+
+    locked_pairs: int = 0
+    seconds: float = 0.0
+    device_ms: float = 0.0
+    launches: int = 0
+
+
+def generate_plan(cds: CDS, defaults: PlanDefaults | None = None, top_subtrees: int | None = None) -> EvalPlan:
+    """Deterministic plan selection following executor.cpp:259-272."""
+    d = defaults or PlanDefaults()
+    import os
+
+    num_leaves = int(cds.leaves().shape[0])
+    plan = EvalPlan()
+    plan.block_threshold = d.block_threshold or num_leaves
+    plan.coarsen_threshold = d.coarsen_threshold
+    plan.p = d.p or (os.cpu_count() or 1)
+    plan.block_lowering_near = cds.num_near > plan.block_threshold
+    plan.block_lowering_far = cds.num_far > plan.block_threshold
+    plan.coarsen_lowering = cds.height + 1 > plan.coarsen_threshold
+    plan.peel_top = plan.coarsen_lowering and top_subtrees is not None and top_subtrees < plan.p
+    return plan
+
+
+def plan_pseudocode(plan: EvalPlan | None = None) -> str:
+    """The loop structure the B200 evaluator runs (cf. executor.cpp:485-514)."""
+    return (
+        "plan(b200: level-batched grouped FP64 GEMM, one CTA per 64x64 output tile)\n"
+        "launch gather: Wp = W[perm, :]\n"
+        "pass upward:\n"
+        "  for height = 0 .. H: one launch over active nodes: T[i] = V[i]^T * (leaf ? Wp[i] : [T[lc]; T[rc]])\n"
+        "pass far + downward:\n"
+        "  for depth = 0 .. H: one launch over active nodes: S[c] = sum_j B[c,j] * T[j] + V[p][c rows] * S[p]\n"
+        "pass near + leaf downward:\n"
+        "  one launch over leaves: Y[i] = U[i] * S[i] + sum_j D[i,j] * W[j]\n"
+        "launch scatter: Y[perm, :] = Y'\n"
+    )
+
+
+class Context:
+    """``hmxg_ctx`` over device ids (repeats allowed: one column shard per entry)."""
+
+    def __init__(self, devices=(0,)):
+        lib = N.hmxg()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(lib.hmxg_create(devs, len(devices), C.byref(h)))
+        self._h = h
+        self.devices = tuple(devices)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if self._h:
+            N.hmxg().hmxg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Evaluator:
+    """A CDS resident on the devices of a context (``hmxg_upload``)."""
+
+    def __init__(self, cds: CDS, devices=(0,), context: Context | None = None):
+        self.cds = cds
+        self.ctx = context or Context(devices)
+        self._own_ctx = context is None
+        h = C.c_void_p()
+        v = cds.view()
+        _check(N.hmxg().hmxg_upload(self.ctx.handle, C.byref(v), C.byref(h)))
+        self._h = h
+        self._lock = threading.Lock()
+
+    def info(self) -> N.Info:
+        inf = N.Info()
+        _check(N.hmxg().hmxg_info_get(self._h, C.byref(inf)))
+        return inf
+
+    def evaluate(self, w: np.ndarray, stats: EvalStats | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        """Y = K~ W with host arrays (column major, float64)."""
+        if w.ndim != 2:
+            raise ValueError("evaluate: W must be a 2-D matrix")
+        n, q = w.shape
+        if n != self.cds.n:
+            raise ValueError("evaluate: W row count does not match the point count")
+        wf = np.asfortranarray(w, dtype=np.float64)
+        y = out if out is not None else np.empty((n, q), dtype=np.float64, order="F")
+        if y.shape != (n, q) or y.dtype != np.float64 or not y.flags.f_contiguous:
+            raise ValueError("evaluate: out must be an n x q Fortran-ordered float64 array")
+        st = N.Stats()
+        if q:
+            _check(N.hmxg().hmxg_evaluate(self._h, wf.ctypes.data_as(C.c_void_p), n, q, n,
+                                          y.ctypes.data_as(C.c_void_p), n, 0, None, C.byref(st)))
+        if stats is not None:
+            stats.locked_pairs = int(st.locked_pairs)
+            stats.seconds = float(st.seconds)
+            stats.device_ms = float(st.device_ms)
+            stats.launches = int(st.launches)
+        return y
+
+    def evaluate_device(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
+                        stream: int = 0, sync: bool = False, stats: EvalStats | None = None) -> None:
+        """Device-pointer evaluation (single-device context): W/Y already in HBM,
+        enqueued on ``stream`` (a cudaStream_t as int, 0 = internal stream)."""
+        n = self.cds.n
+        flags = N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC)
+        st = N.Stats()
+        _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
+                                      flags, C.c_void_p(stream) if stream else None, C.byref(st)))
+        if stats is not None:
+            stats.device_ms = float(st.device_ms)
+            stats.launches = int(st.launches)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.hmxg().hmxg_free(self._h)
+            self._h = None
+        if self._own_ctx and self.ctx is not None:
+            self.ctx.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _evaluator_for(cds: CDS, devices=(0,)) -> Evaluator:
+    key = ("evaluator", tuple(devices))
+    ev = cds._cache.get(key)
+    if ev is None:
+        ev = Evaluator(cds, devices)
+        cds._cache[key] = ev
+    return ev
+
+
+def evaluate(cds: CDS, plan: EvalPlan | None, w: np.ndarray, stats: EvalStats | None = None,
+             devices=(0,)) -> np.ndarray:
+    """``hmx::evaluate(cds, plan, w, &stats)`` on the B200 (executor.cpp:274-302).
+
+    The CDS is uploaded on first use and stays resident (cached on the CDS object).
+    """
+    if w.ndim != 2 or w.shape[0] != cds.n:
+        raise ValueError("evaluate: W row count does not match the point count")
+    if w.shape[1] == 0:
+        if stats is not None:
+            stats.locked_pairs, stats.seconds = 0, 0.0
+        return np.zeros((cds.n, 0), dtype=np.float64, order="F")
+    return _evaluator_for(cds, devices).evaluate(w, stats)
