@@ -28,9 +28,10 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   if (!v.parent || !v.lchild || !v.rchild || !v.start || !v.end || !v.level || !v.perm ||
       !v.sranks || !v.participating || !v.dptr || !v.bptr || !v.vptr)
     return fail(err, "cds: null array in view");
-  if ((v.num_near && (!v.near_pairs || !v.dgen)) || (v.num_far && (!v.far_pairs || !v.bgen)) ||
-      (v.num_v && (!v.v_order || !v.vgen)))
-    return fail(err, "cds: null pair list or generator array in view");
+  if ((v.num_near && !v.near_pairs) || (v.num_far && !v.far_pairs) || (v.num_v && !v.v_order))
+    return fail(err, "cds: null pair list in view");
+  if ((v.dptr[v.num_near] && !v.dgen) || (v.bptr[v.num_far] && !v.bgen) || (v.vptr[v.num_v] && !v.vgen))
+    return fail(err, "cds: null generator array in view");
   if (v.n == 0 || v.n > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: point count out of range");
   if (v.parent[0] != HMXG_NO_NODE || v.start[0] != 0 || v.end[0] != v.n)

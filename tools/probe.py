@@ -15,16 +15,17 @@ for name in sys.argv[1:] or ["cfg1-hss", "cfg5-hss"]:
     ev = Evaluator(c)
     w = torch.randn(q, c.n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(w)
-    s = torch.cuda.current_stream()
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
     for _ in range(3):
         ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 10
-    e0.record()
+    e0.record(s)
     for _ in range(reps):
         ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream)
-    e1.record(); torch.cuda.synchronize()
+    e1.record(s); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     fl = c.flops(q); by = c.bytes(q)
     print(f"{name}: q={q} {ms:.3f} ms  {fl/ms/1e6:.1f} GFLOP/s  frac_fp64={fl/ms/1e9/PEAK*1e3*1e-3:.3f} "
