@@ -33,6 +33,8 @@ extern "C" {
 /* hmxg_evaluate flags */
 #define HMXG_F_DEVICE_PTRS 0x1u /* W and Y are device pointers on the matrix's (single) device */
 #define HMXG_F_NO_SYNC 0x2u     /* with DEVICE_PTRS: enqueue on `stream` and return */
+#define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0);
+                                   read back with hmxg_phase_get */
 
 /*
  * View of a computation-ordered CDS (reference struct hmx::CDS,
@@ -94,6 +96,22 @@ typedef struct hmxg_info {
   uint64_t device_bytes;              /* resident generator + table bytes per device */
 } hmxg_info;
 
+/* One launch of the per-evaluation launch sequence (SURVEY §7.3 / DESIGN.md):
+ * kind 0 gather, 1 upward (level = subtree height), 2 far+downward (level = depth),
+ * 3 near+leaf-downward, 4 scatter. Byte/flop fields are ALGORITHMIC (each operand block
+ * counted once): the roofline numerators of bench.py. last_ms is the device time of that
+ * launch in the last evaluation run with HMXG_F_TIME_PHASES on device 0. */
+typedef struct hmxg_phase {
+  uint32_t kind;
+  uint32_t level;
+  uint32_t tiles;            /* row tiles (grid.x); grid.y = ceil(q / 64) */
+  uint32_t reserved;
+  double flops_per_col;
+  double gen_bytes;          /* generator bytes read once per evaluation */
+  double io_bytes_per_col;   /* operand rows read + output rows written, per column */
+  double last_ms;
+} hmxg_phase;
+
 typedef struct hmxg_ctx hmxg_ctx;
 typedef struct hmxg_mat hmxg_mat;
 
@@ -121,6 +139,11 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info);
  * q == 0 is a no-op (Y is n x 0); a row mismatch (n != cds.n) is HMXG_EINVAL. */
 int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y,
                   size_t ldy, unsigned flags, void* stream, hmxg_stats* stats);
+
+/* Launch sequence description; phase_get synchronizes the timing events of the last
+ * HMXG_F_TIME_PHASES evaluation before filling last_ms. */
+int hmxg_phase_count(const hmxg_mat* mat);
+int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out);
 
 const char* hmxg_last_error(void);
 const char* hmxg_version(void);

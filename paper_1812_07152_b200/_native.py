@@ -20,6 +20,8 @@ HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM = 0, 1, 2, 3, 4
 HMXG_NO_NODE = 0xFFFFFFFF
 HMXG_F_DEVICE_PTRS = 0x1
 HMXG_F_NO_SYNC = 0x2
+HMXG_F_TIME_PHASES = 0x4
+PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter"}
 
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
@@ -88,6 +90,21 @@ class Info(C.Structure):
     ]
 
 
+class Phase(C.Structure):
+    """``hmxg_phase``."""
+
+    _fields_ = [
+        ("kind", C.c_uint32),
+        ("level", C.c_uint32),
+        ("tiles", C.c_uint32),
+        ("reserved", C.c_uint32),
+        ("flops_per_col", C.c_double),
+        ("gen_bytes", C.c_double),
+        ("io_bytes_per_col", C.c_double),
+        ("last_ms", C.c_double),
+    ]
+
+
 class BuildSpec(C.Structure):
     """``hmxb_spec`` (include/hmxb.h)."""
 
@@ -150,6 +167,8 @@ HMXG_SYMBOLS = {
         [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_size_t,
          C.c_uint, C.c_void_p, C.POINTER(Stats)],
     ),
+    "hmxg_phase_count": (C.c_int, [C.c_void_p]),
+    "hmxg_phase_get": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(Phase)]),
     "hmxg_last_error": (C.c_char_p, []),
     "hmxg_version": (C.c_char_p, []),
 }

@@ -1,5 +1,6 @@
 // hmxg.cu — C-ABI of the B200 evaluator (include/hmxg.h): device residency of the CDS,
-// workspace management, column sharding over devices and the launch sequence.
+// workspace management, column sharding over devices, the launch sequence and the
+// pipelined host<->device path.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,15 +26,21 @@ int set_err(int code, const std::string& msg) {
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
-  cudaGetLastError();  // clear sticky-free errors
+  cudaGetLastError();  // clear non-sticky errors
   return set_err(e == cudaErrorMemoryAllocation ? HMXG_ENOMEM : HMXG_ECUDA,
                  std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define HMXG_CUDA(call)                                   \
-  do {                                                    \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+#define HMXG_CUDA(call)                                 \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+#define HMXG_TRY(call)          \
+  do {                          \
+    int rc_ = (call);           \
+    if (rc_ != HMXG_OK) return rc_; \
   } while (0)
 
 template <class T>
@@ -45,10 +52,17 @@ int dev_upload(T** dst, const T* src, std::size_t count, cudaStream_t st) {
   return HMXG_OK;
 }
 
+// Columns per pipeline chunk of the host-pointer path: H2D of chunk k+1 and D2H of chunk
+// k-1 overlap the evaluation of chunk k.
+constexpr std::size_t kChunkCols = 256;
+
 struct DevState {
   int dev = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> phase_ev;  // launches + 1
+  bool phase_valid = false;
   double* gen[3] = {nullptr, nullptr, nullptr};
   Task* tasks = nullptr;
   Seg* segs = nullptr;
@@ -59,9 +73,9 @@ struct DevState {
   double* yp = nullptr;
   double* t = nullptr;
   double* s = nullptr;
-  std::size_t stage_q = 0;  // host-mode staging capacity in columns
-  double* w_stage = nullptr;
-  double* y_stage = nullptr;
+  std::size_t stage_q = 0;  // host-path staging capacity (columns per buffer)
+  double* w_stage[2] = {nullptr, nullptr};
+  double* y_stage[2] = {nullptr, nullptr};
   std::uint64_t resident_bytes = 0;
 
   void release_workspace() {
@@ -73,14 +87,17 @@ struct DevState {
     cap_q = 0;
   }
   void release_stage() {
-    cudaFree(w_stage);
-    cudaFree(y_stage);
-    w_stage = y_stage = nullptr;
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(w_stage[b]);
+      cudaFree(y_stage[b]);
+      w_stage[b] = y_stage[b] = nullptr;
+    }
     stage_q = 0;
   }
   void release() {
     if (cudaSetDevice(dev) != cudaSuccess) return;
-    if (stream) cudaStreamSynchronize(stream);
+    for (cudaStream_t st : {comp, h2d, d2h})
+      if (st) cudaStreamSynchronize(st);
     release_workspace();
     release_stage();
     for (auto*& g : gen) {
@@ -94,11 +111,12 @@ struct DevState {
     tasks = nullptr;
     segs = nullptr;
     perm = iperm = nullptr;
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
-    ev0 = ev1 = nullptr;
-    stream = nullptr;
+    for (cudaEvent_t* e : {&ev0, &ev1, &ev_in[0], &ev_in[1], &ev_done[0], &ev_done[1], &ev_out[0], &ev_out[1]})
+      if (*e) cudaEventDestroy(*e), *e = nullptr;
+    for (auto& e : phase_ev) cudaEventDestroy(e);
+    phase_ev.clear();
+    for (cudaStream_t* st : {&comp, &h2d, &d2h})
+      if (*st) cudaStreamDestroy(*st), *st = nullptr;
   }
 };
 
@@ -134,21 +152,31 @@ int ensure_workspace(const Plan& plan, DevState& d, std::size_t q) {
 int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
   if (q <= d.stage_q) return HMXG_OK;
   d.release_stage();
-  HMXG_CUDA(cudaMalloc(&d.w_stage, plan.n * q * sizeof(double)));
-  HMXG_CUDA(cudaMalloc(&d.y_stage, plan.n * q * sizeof(double)));
+  for (int b = 0; b < 2; ++b) {
+    HMXG_CUDA(cudaMalloc(&d.w_stage[b], plan.n * q * sizeof(double)));
+    HMXG_CUDA(cudaMalloc(&d.y_stage[b], plan.n * q * sizeof(double)));
+  }
   d.stage_q = q;
   return HMXG_OK;
 }
 
-// Enqueue one full evaluation of q columns on d.stream: W (ldw) -> Y (ldy), device ptrs.
+// Enqueue one full evaluation of q columns: W (ldw) -> Y (ldy), device pointers.
 int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw, double* y,
-                 std::size_t ldy, std::size_t q, cudaStream_t st, std::uint32_t* launches) {
+                 std::size_t ldy, std::size_t q, cudaStream_t st, bool time_phases,
+                 std::uint32_t* launches) {
   const std::uint32_t n = static_cast<std::uint32_t>(plan.n);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
   const dim3 eblk(256);
   const dim3 egrid((n + 255) / 256, std::min<std::uint32_t>(qq, 65535));
+  std::size_t ev = 0;
+  auto mark = [&]() -> int {
+    if (time_phases) HMXG_CUDA(cudaEventRecord(d.phase_ev[ev++], st));
+    return HMXG_OK;
+  };
+  HMXG_TRY(mark());
   gather_rows<<<egrid, eblk, 0, st>>>(w, ldw, d.perm, d.wp, plan.n, n, qq);
   ++*launches;
+  HMXG_TRY(mark());
 
   EvalParams p{};
   p.gen[kGenD] = d.gen[kGenD];
@@ -173,10 +201,56 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     else
       grouped_gemm<false><<<grid, kThreads, kSmemBytes, st>>>(p);
     ++*launches;
+    HMXG_TRY(mark());
   }
   scatter_rows<<<egrid, eblk, 0, st>>>(d.yp, plan.n, d.iperm, y, ldy, n, qq);
   ++*launches;
+  HMXG_TRY(mark());
   HMXG_CUDA(cudaGetLastError());
+  if (time_phases) d.phase_valid = true;
+  return HMXG_OK;
+}
+
+int copy_cols(double* dst, std::size_t lddst, const double* src, std::size_t ldsrc, std::size_t rows,
+              std::size_t cols, cudaMemcpyKind kind, cudaStream_t st) {
+  if (lddst == rows && ldsrc == rows) {
+    HMXG_CUDA(cudaMemcpyAsync(dst, src, rows * cols * sizeof(double), kind, st));
+  } else {
+    HMXG_CUDA(cudaMemcpy2DAsync(dst, lddst * sizeof(double), src, ldsrc * sizeof(double), rows * sizeof(double),
+                                cols, kind, st));
+  }
+  return HMXG_OK;
+}
+
+// Host-pointer evaluation of columns [c0, c1) on device d: chunks of kChunkCols columns,
+// double-buffered staging, copies on their own streams so PCIe traffic in both
+// directions overlaps the kernels.
+int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size_t ldw, double* Y,
+                       std::size_t ldy, std::size_t c0, std::size_t c1, bool time_phases,
+                       std::uint32_t* launches) {
+  const std::size_t n = plan.n, qg = c1 - c0;
+  const std::size_t cq = std::min(qg, kChunkCols);
+  HMXG_TRY(ensure_workspace(plan, d, cq));
+  HMXG_TRY(ensure_stage(plan, d, cq));
+  const std::size_t chunks = (qg + cq - 1) / cq;
+  for (std::size_t k = 0; k < chunks; ++k) {
+    const int b = static_cast<int>(k & 1);
+    const std::size_t a = c0 + k * cq, m = std::min(cq, c1 - a);
+    // input buffer b is free once the evaluation of chunk k-2 finished
+    if (k >= 2) HMXG_CUDA(cudaStreamWaitEvent(d.h2d, d.ev_done[b], 0));
+    HMXG_TRY(copy_cols(d.w_stage[b], n, W + a * ldw, ldw, n, m, cudaMemcpyHostToDevice, d.h2d));
+    HMXG_CUDA(cudaEventRecord(d.ev_in[b], d.h2d));
+    HMXG_CUDA(cudaStreamWaitEvent(d.comp, d.ev_in[b], 0));
+    // output buffer b is free once the copy-out of chunk k-2 finished
+    if (k >= 2) HMXG_CUDA(cudaStreamWaitEvent(d.comp, d.ev_out[b], 0));
+    if (k == 0) HMXG_CUDA(cudaEventRecord(d.ev0, d.comp));
+    HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, time_phases && k == 0, launches));
+    HMXG_CUDA(cudaEventRecord(d.ev_done[b], d.comp));
+    if (k + 1 == chunks) HMXG_CUDA(cudaEventRecord(d.ev1, d.comp));
+    HMXG_CUDA(cudaStreamWaitEvent(d.d2h, d.ev_done[b], 0));
+    HMXG_TRY(copy_cols(Y + a * ldy, ldy, d.y_stage[b], n, n, m, cudaMemcpyDeviceToHost, d.d2h));
+    HMXG_CUDA(cudaEventRecord(d.ev_out[b], d.d2h));
+  }
   return HMXG_OK;
 }
 
@@ -188,24 +262,23 @@ using namespace hmxg;
 extern "C" {
 
 const char* hmxg_last_error(void) { return g_err.c_str(); }
-const char* hmxg_version(void) { return "hmxg 0.1 sm_100a fp64-dmma grouped-gemm"; }
+const char* hmxg_version(void) { return "hmxg 0.2 sm_100a fp64-dmma grouped-gemm"; }
 
 int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
   if (!out) return set_err(HMXG_EINVAL, "hmxg_create: null out");
   *out = nullptr;
   int count = 0;
   HMXG_CUDA(cudaGetDeviceCount(&count));
+  if (count == 0) return set_err(HMXG_ECUDA, "hmxg_create: no CUDA device");
   auto ctx = std::make_unique<hmxg_ctx>();
   if (ndev <= 0 || !devs) {
     ctx->devs.push_back(0);
   } else {
     for (int i = 0; i < ndev; ++i) {
-      if (devs[i] < 0 || devs[i] >= count)
-        return set_err(HMXG_EINVAL, "hmxg_create: device id out of range");
+      if (devs[i] < 0 || devs[i] >= count) return set_err(HMXG_EINVAL, "hmxg_create: device id out of range");
       ctx->devs.push_back(devs[i]);
     }
   }
-  if (count == 0) return set_err(HMXG_ECUDA, "hmxg_create: no CUDA device");
   for (int dv : ctx->devs) {
     cudaDeviceProp prop{};
     HMXG_CUDA(cudaGetDeviceProperties(&prop, dv));
@@ -217,42 +290,6 @@ int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
 
 int hmxg_destroy(hmxg_ctx* ctx) {
   delete ctx;
-  return HMXG_OK;
-}
-
-int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
-  if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
-  *out = nullptr;
-  auto mat = std::make_unique<hmxg_mat>();
-  mat->ctx = ctx;
-  std::string err;
-  if (!build_plan(*cds, kBM, mat->plan, err)) return set_err(HMXG_EINVAL, err);
-  const Plan& plan = mat->plan;
-  std::vector<std::uint32_t> iperm(plan.n);
-  for (std::uint64_t pos = 0; pos < plan.n; ++pos) iperm[cds->perm[pos]] = static_cast<std::uint32_t>(pos);
-  mat->devs.resize(ctx->devs.size());
-  for (std::size_t g = 0; g < ctx->devs.size(); ++g) {
-    DevState& d = mat->devs[g];
-    d.dev = ctx->devs[g];
-    HMXG_CUDA(cudaSetDevice(d.dev));
-    HMXG_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    HMXG_CUDA(cudaEventCreate(&d.ev0));
-    HMXG_CUDA(cudaEventCreate(&d.ev1));
-    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    int rc;
-    if ((rc = dev_upload(&d.gen[kGenD], cds->dgen, plan.d_elems, d.stream))) return rc;
-    if ((rc = dev_upload(&d.gen[kGenB], cds->bgen, plan.b_elems, d.stream))) return rc;
-    if ((rc = dev_upload(&d.gen[kGenV], cds->vgen, plan.v_elems, d.stream))) return rc;
-    if ((rc = dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.stream))) return rc;
-    if ((rc = dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.stream))) return rc;
-    if ((rc = dev_upload(&d.perm, cds->perm, plan.n, d.stream))) return rc;
-    if ((rc = dev_upload(&d.iperm, iperm.data(), plan.n, d.stream))) return rc;
-    HMXG_CUDA(cudaStreamSynchronize(d.stream));
-    d.resident_bytes = 8 * (plan.d_elems + plan.b_elems + plan.v_elems) +
-                       sizeof(Task) * plan.tasks.size() + sizeof(Seg) * plan.segs.size() + 8 * plan.n;
-  }
-  *out = mat.release();
   return HMXG_OK;
 }
 
@@ -271,6 +308,45 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
     info->launches_per_eval = static_cast<std::uint32_t>(plan.phases.size() + 2);
     info->flops_per_col = 2.0 * (2.0 * plan.v_elems + plan.b_elems + plan.d_elems);
   }
+  return HMXG_OK;
+}
+
+int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
+  if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
+  *out = nullptr;
+  auto mat = std::make_unique<hmxg_mat>();
+  mat->ctx = ctx;
+  std::string err;
+  if (!build_plan(*cds, kBM, mat->plan, err)) return set_err(HMXG_EINVAL, err);
+  const Plan& plan = mat->plan;
+  std::vector<std::uint32_t> iperm(plan.n);
+  for (std::uint64_t pos = 0; pos < plan.n; ++pos) iperm[cds->perm[pos]] = static_cast<std::uint32_t>(pos);
+  mat->devs.resize(ctx->devs.size());
+  for (std::size_t g = 0; g < ctx->devs.size(); ++g) {
+    DevState& d = mat->devs[g];
+    d.dev = ctx->devs[g];
+    HMXG_CUDA(cudaSetDevice(d.dev));
+    for (cudaStream_t* st : {&d.comp, &d.h2d, &d.d2h}) HMXG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&d.ev0, &d.ev1}) HMXG_CUDA(cudaEventCreate(e));
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
+        HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    d.phase_ev.resize(plan.phases.size() + 3);
+    for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
+    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_TRY(dev_upload(&d.gen[kGenD], cds->dgen, plan.d_elems, d.comp));
+    HMXG_TRY(dev_upload(&d.gen[kGenB], cds->bgen, plan.b_elems, d.comp));
+    HMXG_TRY(dev_upload(&d.gen[kGenV], cds->vgen, plan.v_elems, d.comp));
+    HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.perm, cds->perm, plan.n, d.comp));
+    HMXG_TRY(dev_upload(&d.iperm, iperm.data(), plan.n, d.comp));
+    HMXG_CUDA(cudaStreamSynchronize(d.comp));
+    d.resident_bytes = 8 * (plan.d_elems + plan.b_elems + plan.v_elems) + sizeof(Task) * plan.tasks.size() +
+                       sizeof(Seg) * plan.segs.size() + 8 * plan.n;
+  }
+  *out = mat.release();
   return HMXG_OK;
 }
 
@@ -297,18 +373,53 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   return HMXG_OK;
 }
 
-int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y,
-                  size_t ldy, unsigned flags, void* stream, hmxg_stats* stats) {
+int hmxg_phase_count(const hmxg_mat* mat) {
+  return mat ? static_cast<int>(mat->plan.phases.size() + 2) : -1;
+}
+
+int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
+  if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
+  const Plan& p = mat->plan;
+  const std::uint32_t count = static_cast<std::uint32_t>(p.phases.size() + 2);
+  if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
+  std::memset(out, 0, sizeof *out);
+  if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
+    out->kind = idx == 0 ? 0 : 4;
+    out->tiles = static_cast<std::uint32_t>((p.n + 255) / 256);
+    out->io_bytes_per_col = 16.0 * p.n;
+    out->gen_bytes = 4.0 * p.n;  // the permutation itself
+  } else {
+    const Phase& ph = p.phases[idx - 1];
+    out->kind = ph.kind == kPhaseUp ? 1 : (ph.kind == kPhaseDown ? 2 : 3);
+    out->level = ph.level;
+    out->tiles = ph.task_end - ph.task_begin;
+    out->flops_per_col = ph.flops_per_col;
+    out->gen_bytes = ph.gen_bytes;
+    out->io_bytes_per_col = ph.io_bytes_per_col;
+  }
+  DevState& d = mat->devs[0];
+  if (d.phase_valid) {
+    HMXG_CUDA(cudaSetDevice(d.dev));
+    HMXG_CUDA(cudaEventSynchronize(d.phase_ev[idx + 1]));
+    float ms = 0.f;
+    HMXG_CUDA(cudaEventElapsedTime(&ms, d.phase_ev[idx], d.phase_ev[idx + 1]));
+    out->last_ms = ms;
+  }
+  return HMXG_OK;
+}
+
+int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y, size_t ldy,
+                  unsigned flags, void* stream, hmxg_stats* stats) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!mat) return set_err(HMXG_EINVAL, "hmxg_evaluate: null matrix");
-  if (n != mat->plan.n)
-    return set_err(HMXG_EINVAL, "evaluate: W row count does not match the point count");
+  if (n != mat->plan.n) return set_err(HMXG_EINVAL, "evaluate: W row count does not match the point count");
   if (stats) std::memset(stats, 0, sizeof *stats);
   if (q == 0) return HMXG_OK;  // executor.cpp:279-282
   if (!W || !Y || ldw < n || ldy < n) return set_err(HMXG_EINVAL, "hmxg_evaluate: bad W/Y or leading dimension");
   if (q > 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns");
   std::lock_guard<std::mutex> lock(mat->mu);
   const Plan& plan = mat->plan;
+  const bool time_phases = flags & HMXG_F_TIME_PHASES;
   std::uint32_t launches = 0;
   float dev_ms = 0.f;
 
@@ -317,12 +428,11 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       return set_err(HMXG_EINVAL, "hmxg_evaluate: device pointers need a single-device context");
     DevState& d = mat->devs[0];
     HMXG_CUDA(cudaSetDevice(d.dev));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
-    int rc = ensure_workspace(plan, d, q);
-    if (rc) return rc;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.comp;
+    HMXG_TRY(ensure_workspace(plan, d, q));
     const bool sync = !(flags & HMXG_F_NO_SYNC);
     if (sync) HMXG_CUDA(cudaEventRecord(d.ev0, st));
-    if ((rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, &launches))) return rc;
+    HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, &launches));
     if (sync) {
       HMXG_CUDA(cudaEventRecord(d.ev1, st));
       HMXG_CUDA(cudaEventSynchronize(d.ev1));
@@ -331,29 +441,20 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
   } else {
     // column sharding over the context's devices: Y[:,c] depends only on W[:,c]
     const std::size_t G = mat->devs.size();
-    std::vector<std::size_t> c0(G + 1);
-    for (std::size_t g = 0; g <= G; ++g) c0[g] = q * g / G;
+    std::vector<std::size_t> cut(G + 1);
+    for (std::size_t g = 0; g <= G; ++g) cut[g] = q * g / G;
     for (std::size_t g = 0; g < G; ++g) {
+      if (cut[g + 1] == cut[g]) continue;
       DevState& d = mat->devs[g];
-      const std::size_t qg = c0[g + 1] - c0[g];
-      if (qg == 0) continue;
       HMXG_CUDA(cudaSetDevice(d.dev));
-      int rc = ensure_workspace(plan, d, qg);
-      if (!rc) rc = ensure_stage(plan, d, qg);
-      if (rc) return rc;
-      HMXG_CUDA(cudaMemcpy2DAsync(d.w_stage, n * sizeof(double), W + c0[g] * ldw, ldw * sizeof(double),
-                                  n * sizeof(double), qg, cudaMemcpyHostToDevice, d.stream));
-      HMXG_CUDA(cudaEventRecord(d.ev0, d.stream));
-      if ((rc = enqueue_eval(plan, d, d.w_stage, n, d.y_stage, n, qg, d.stream, &launches))) return rc;
-      HMXG_CUDA(cudaEventRecord(d.ev1, d.stream));
-      HMXG_CUDA(cudaMemcpy2DAsync(Y + c0[g] * ldy, ldy * sizeof(double), d.y_stage, n * sizeof(double),
-                                  n * sizeof(double), qg, cudaMemcpyDeviceToHost, d.stream));
+      HMXG_TRY(enqueue_host_shard(plan, d, W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0, &launches));
     }
     for (std::size_t g = 0; g < G; ++g) {
+      if (cut[g + 1] == cut[g]) continue;
       DevState& d = mat->devs[g];
-      if (c0[g + 1] == c0[g]) continue;
       HMXG_CUDA(cudaSetDevice(d.dev));
-      HMXG_CUDA(cudaStreamSynchronize(d.stream));
+      HMXG_CUDA(cudaStreamSynchronize(d.d2h));
+      HMXG_CUDA(cudaStreamSynchronize(d.comp));
       float ms = 0.f;
       HMXG_CUDA(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
       dev_ms = std::max(dev_ms, ms);

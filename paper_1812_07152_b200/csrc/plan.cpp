@@ -142,8 +142,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   plan.skel_rows = rows;
 
   const std::uint32_t bm = tile_m;
-  auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs,
-                       double& phase_flops) {
+  auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs, Phase& ph) {
     const std::uint32_t tiles = m == 0 ? 0 : (m + bm - 1) / bm;
     for (std::uint32_t t = 0; t < tiles; ++t) {
       const std::uint32_t r0 = t * bm;
@@ -154,10 +153,14 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       task.seg_begin = static_cast<std::uint32_t>(plan.segs.size());
       emit_segs(r0);
       task.seg_end = static_cast<std::uint32_t>(plan.segs.size());
-      for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s)
-        phase_flops += 2.0 * task.m * plan.segs[s].k;
+      for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s) {
+        ph.flops_per_col += 2.0 * task.m * plan.segs[s].k;
+        ph.gen_bytes += 8.0 * task.m * plan.segs[s].k;
+        if (t == 0) ph.io_bytes_per_col += 8.0 * plan.segs[s].k;  // B rows, read once per node
+      }
       plan.tasks.push_back(task);
     }
+    ph.io_bytes_per_col += 8.0 * m;  // C rows, written once
     plan.max_m = std::max(plan.max_m, m);
   };
   auto push_seg = [&](Gen gen, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k, Buf bbuf,
@@ -168,7 +171,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
                             static_cast<std::uint16_t>(bbuf)});
   };
   auto open_phase = [&](PhaseKind kind, bool trans, std::uint32_t level) {
-    plan.phases.push_back(Phase{kind, trans, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0});
+    plan.phases.push_back(Phase{kind, trans, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0, 0.0, 0.0});
   };
   auto close_phase = [&]() {
     Phase& ph = plan.phases.back();
@@ -190,7 +193,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
           push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufWp, v.start[i]);
         else
           push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufT, plan.node_off[v.lchild[i]]);
-      }, plan.phases.back().flops_per_col);
+      }, plan.phases.back());
     }
     close_phase();
   }
@@ -212,7 +215,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
           push_seg(kGenV, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], kBufS,
                    plan.node_off[p]);
         }
-      }, plan.phases.back().flops_per_col);
+      }, plan.phases.back());
     }
     close_phase();
   }
@@ -228,7 +231,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         const std::uint32_t j = v.near_pairs[2 * s + 1];
         push_seg(kGenD, v.dptr[s] + r0, m, size_of(j), kBufWp, v.start[j]);
       }
-    }, plan.phases.back().flops_per_col);
+    }, plan.phases.back());
   }
   close_phase();
   if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())

@@ -63,6 +63,8 @@ struct Phase {
   std::uint32_t task_begin, task_end;
   std::uint32_t level;   // height (up) or depth (down)
   double flops_per_col;  // 2*sum(m*k) over the phase's tiles, algorithmic
+  double gen_bytes;      // generator (A operand) bytes the phase reads once per evaluation
+  double io_bytes_per_col;  // B operand rows read + C rows written, once per node, per column
 };
 
 struct Plan {

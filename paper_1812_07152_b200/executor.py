@@ -150,6 +150,32 @@ class Evaluator:
         _check(N.hmxg().hmxg_info_get(self._h, C.byref(inf)))
         return inf
 
+    def phases(self) -> list[dict]:
+        """The launch sequence with algorithmic flops/bytes and, after an evaluation run
+        with ``time_phases=True``, the device time of every launch (device 0)."""
+        lib = N.hmxg()
+        out = []
+        for i in range(lib.hmxg_phase_count(self._h)):
+            ph = N.Phase()
+            _check(lib.hmxg_phase_get(self._h, i, C.byref(ph)))
+            out.append({"kind": N.PHASE_KINDS[ph.kind], "level": ph.level, "tiles": ph.tiles,
+                        "flops_per_col": ph.flops_per_col, "gen_bytes": ph.gen_bytes,
+                        "io_bytes_per_col": ph.io_bytes_per_col, "ms": ph.last_ms})
+        return out
+
+    def evaluate_host_ptr(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
+                          time_phases: bool = False, stats: EvalStats | None = None) -> None:
+        """Host-pointer evaluation (pinned buffers give overlapped PCIe transfers)."""
+        n = self.cds.n
+        st = N.Stats()
+        flags = N.HMXG_F_TIME_PHASES if time_phases else 0
+        _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
+                                      flags, None, C.byref(st)))
+        if stats is not None:
+            stats.seconds = float(st.seconds)
+            stats.device_ms = float(st.device_ms)
+            stats.launches = int(st.launches)
+
     def evaluate(self, w: np.ndarray, stats: EvalStats | None = None, out: np.ndarray | None = None) -> np.ndarray:
         """Y = K~ W with host arrays (column major, float64)."""
         if w.ndim != 2:
@@ -173,11 +199,12 @@ class Evaluator:
         return y
 
     def evaluate_device(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
-                        stream: int = 0, sync: bool = False, stats: EvalStats | None = None) -> None:
+                        stream: int = 0, sync: bool = False, stats: EvalStats | None = None,
+                        time_phases: bool = False) -> None:
         """Device-pointer evaluation (single-device context): W/Y already in HBM,
         enqueued on ``stream`` (a cudaStream_t as int, 0 = internal stream)."""
         n = self.cds.n
-        flags = N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC)
+        flags = N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC) | (N.HMXG_F_TIME_PHASES if time_phases else 0)
         st = N.Stats()
         _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
                                       flags, C.c_void_p(stream) if stream else None, C.byref(st)))
