@@ -193,7 +193,7 @@ def reference_arm(args) -> None:
     _, q_total = config(args.config)
     threads = os.cpu_count() or 1
     res = run_reference(args.config, args.steps, args.warmup, args.ref_step_s, threads,
-                        timeout=max(120.0, 60.0 * (args.steps + args.warmup)))
+                        timeout=max(90.0, 15.0 * (args.steps + args.warmup) * args.ref_step_s))
     n_gpus = args.gpus
     if "error" in res:
         print(json.dumps({"impl": "reference", "unavailable": "reference evaluate failed: " + res["error"]}))
@@ -345,7 +345,7 @@ def ours(args) -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res = run_reference(args.config, 1, 0, args.cpu_step_s, os.cpu_count() or 1, timeout=300.0)
+        res = run_reference(args.config, 1, 0, args.cpu_step_s, os.cpu_count() or 1, timeout=120.0)
         if "error" not in res:
             v = res["flops_per_step"] / statistics.mean(res["times"]) / 1e9
             cpu = {"value": v, "unit": "GFLOP/s", "cores": res["threads"], "kind": "reference",

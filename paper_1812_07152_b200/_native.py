@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-HMXG_PATH = os.path.join(_HERE, "libhmxg.so")
+HMXG_PATH = os.environ.get("HMXG_LIBRARY") or os.path.join(_HERE, "libhmxg.so")  # override: A/B builds
 HMXB_PATH = os.path.join(_HERE, "libhmxb.so")
 
 HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM = 0, 1, 2, 3, 4

@@ -1,6 +1,7 @@
 // hmxg.cu — C-ABI of the B200 evaluator (include/hmxg.h): device residency of the CDS,
 // workspace management, column sharding over devices, the launch sequence and the
 // pipelined host<->device path.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -52,9 +53,43 @@ int dev_upload(T** dst, const T* src, std::size_t count, cudaStream_t st) {
   return HMXG_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D map over a point-major buffer (rows x q, Q contiguous, row pitch ld): boxes of
+// 16 rows x kBPitch columns, no swizzle (the pitch keeps fragment loads conflict-free),
+// zero fill past column q.
+int make_map(CUtensorMap* map, const double* base, std::uint64_t rows, std::uint64_t cols, std::uint64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_err(HMXG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBPitch), static_cast<cuuint32_t>(kBK)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(HMXG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return HMXG_OK;
+}
+
 // Columns per pipeline chunk of the host-pointer path: H2D of chunk k+1 and D2H of chunk
 // k-1 overlap the evaluation of chunk k.
-constexpr std::size_t kChunkCols = 256;
+constexpr std::size_t kChunkCols = 64;
 
 struct DevState {
   int dev = 0;
@@ -63,12 +98,11 @@ struct DevState {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> phase_ev;  // launches + 1
   bool phase_valid = false;
-  double* gen[3] = {nullptr, nullptr, nullptr};
+  double* tiles = nullptr;  // pre-tiled A operands
   Task* tasks = nullptr;
-  Seg* segs = nullptr;
-  std::uint32_t* perm = nullptr;
-  std::uint32_t* iperm = nullptr;
-  std::size_t cap_q = 0;  // evaluation workspace capacity in columns
+  SegDev* segs = nullptr;
+  std::uint32_t* ipmap = nullptr;
+  std::size_t cap_q = 0;  // evaluation workspace capacity in columns (= row pitch of Wp/T/S/Yp)
   double* wp = nullptr;
   double* yp = nullptr;
   double* t = nullptr;
@@ -100,17 +134,14 @@ struct DevState {
       if (st) cudaStreamSynchronize(st);
     release_workspace();
     release_stage();
-    for (auto*& g : gen) {
-      cudaFree(g);
-      g = nullptr;
-    }
+    cudaFree(tiles);
     cudaFree(tasks);
     cudaFree(segs);
-    cudaFree(perm);
-    cudaFree(iperm);
+    cudaFree(ipmap);
+    tiles = nullptr;
     tasks = nullptr;
     segs = nullptr;
-    perm = iperm = nullptr;
+    ipmap = nullptr;
     for (cudaEvent_t* e : {&ev0, &ev1, &ev_in[0], &ev_in[1], &ev_done[0], &ev_done[1], &ev_out[0], &ev_out[1]})
       if (*e) cudaEventDestroy(*e), *e = nullptr;
     for (auto& e : phase_ev) cudaEventDestroy(e);
@@ -137,14 +168,21 @@ struct hmxg_mat {
 namespace hmxg {
 namespace {
 
+// Wp/Yp/T/S are point-major with a row pitch of cap_q columns (a multiple of 8: 64-byte
+// aligned rows for TMA and the vectorized epilogue).
 int ensure_workspace(const Plan& plan, DevState& d, std::size_t q) {
+  q = (q + 7) / 8 * 8;
   if (q <= d.cap_q) return HMXG_OK;
   d.release_workspace();
-  const std::size_t n = plan.n, r = std::max<std::uint64_t>(plan.skel_rows, 1);
+  const std::size_t n = plan.rows_pad, r = plan.skel_rows;
   HMXG_CUDA(cudaMalloc(&d.wp, n * q * sizeof(double)));
   HMXG_CUDA(cudaMalloc(&d.yp, n * q * sizeof(double)));
   HMXG_CUDA(cudaMalloc(&d.t, r * q * sizeof(double)));
   HMXG_CUDA(cudaMalloc(&d.s, r * q * sizeof(double)));
+  // pad rows of Wp/T/S are read as zeros by the 16-row B chunks and never written
+  HMXG_CUDA(cudaMemset(d.wp, 0, n * q * sizeof(double)));
+  HMXG_CUDA(cudaMemset(d.t, 0, r * q * sizeof(double)));
+  HMXG_CUDA(cudaMemset(d.s, 0, r * q * sizeof(double)));
   d.cap_q = q;
   return HMXG_OK;
 }
@@ -167,43 +205,45 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   const std::uint32_t n = static_cast<std::uint32_t>(plan.n);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
   const dim3 eblk(256);
-  const dim3 egrid((n + 255) / 256, std::min<std::uint32_t>(qq, 65535));
   std::size_t ev = 0;
   auto mark = [&]() -> int {
     if (time_phases) HMXG_CUDA(cudaEventRecord(d.phase_ev[ev++], st));
     return HMXG_OK;
   };
+  CUtensorMap tm_wp, tm_t, tm_s;
+  const std::uint64_t ldq = d.cap_q;
+  HMXG_TRY(make_map(&tm_wp, d.wp, plan.rows_pad, q, ldq));
+  HMXG_TRY(make_map(&tm_t, d.t, plan.skel_rows, q, ldq));
+  HMXG_TRY(make_map(&tm_s, d.s, plan.skel_rows, q, ldq));
   HMXG_TRY(mark());
-  gather_rows<<<egrid, eblk, 0, st>>>(w, ldw, d.perm, d.wp, plan.n, n, qq);
+  const dim3 pgrid((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
+  if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
+  permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
   ++*launches;
   HMXG_TRY(mark());
 
-  EvalParams p{};
-  p.gen[kGenD] = d.gen[kGenD];
-  p.gen[kGenB] = d.gen[kGenB];
-  p.gen[kGenV] = d.gen[kGenV];
+  GemmParams p{};
+  p.tiles = d.tiles;
   p.buf[kBufWp] = d.wp;
   p.buf[kBufT] = d.t;
   p.buf[kBufS] = d.s;
   p.buf[kBufYp] = d.yp;
-  p.ld[kBufWp] = plan.n;
-  p.ld[kBufT] = plan.skel_rows;
-  p.ld[kBufS] = plan.skel_rows;
-  p.ld[kBufYp] = plan.n;
+  p.ld[kBufWp] = ldq;
+  p.ld[kBufT] = ldq;
+  p.ld[kBufS] = ldq;
+  p.ld[kBufYp] = ldq;
   p.segs = d.segs;
   p.q = qq;
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
   for (const Phase& ph : plan.phases) {
     p.tasks = d.tasks + ph.task_begin;
-    const dim3 grid(ph.task_end - ph.task_begin, col_blocks);
-    if (ph.trans_a)
-      grouped_gemm<true><<<grid, kThreads, kSmemBytes, st>>>(p);
-    else
-      grouped_gemm<false><<<grid, kThreads, kSmemBytes, st>>>(p);
+    const std::uint64_t ctas = std::uint64_t(ph.task_end - ph.task_begin) * col_blocks;
+    if (ctas > 0x7fffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: grid too large");
+    grouped_gemm<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p);
     ++*launches;
     HMXG_TRY(mark());
   }
-  scatter_rows<<<egrid, eblk, 0, st>>>(d.yp, plan.n, d.iperm, y, ldy, n, qq);
+  permute_out<<<pgrid, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq);
   ++*launches;
   HMXG_TRY(mark());
   HMXG_CUDA(cudaGetLastError());
@@ -262,7 +302,7 @@ using namespace hmxg;
 extern "C" {
 
 const char* hmxg_last_error(void) { return g_err.c_str(); }
-const char* hmxg_version(void) { return "hmxg 0.2 sm_100a fp64-dmma grouped-gemm"; }
+const char* hmxg_version(void) { return "hmxg 0.3 sm_100a fp64-dmma tma-pipelined grouped-gemm"; }
 
 int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
   if (!out) return set_err(HMXG_EINVAL, "hmxg_create: null out");
@@ -319,8 +359,6 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
   std::string err;
   if (!build_plan(*cds, kBM, mat->plan, err)) return set_err(HMXG_EINVAL, err);
   const Plan& plan = mat->plan;
-  std::vector<std::uint32_t> iperm(plan.n);
-  for (std::uint64_t pos = 0; pos < plan.n; ++pos) iperm[cds->perm[pos]] = static_cast<std::uint32_t>(pos);
   mat->devs.resize(ctx->devs.size());
   for (std::size_t g = 0; g < ctx->devs.size(); ++g) {
     DevState& d = mat->devs[g];
@@ -333,18 +371,35 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
         HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     d.phase_ev.resize(plan.phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
-    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    HMXG_TRY(dev_upload(&d.gen[kGenD], cds->dgen, plan.d_elems, d.comp));
-    HMXG_TRY(dev_upload(&d.gen[kGenB], cds->bgen, plan.b_elems, d.comp));
-    HMXG_TRY(dev_upload(&d.gen[kGenV], cds->vgen, plan.v_elems, d.comp));
+    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    // raw generators -> pre-tiled A operands on the device, then the raw copies go away
+    double *gd = nullptr, *gb = nullptr, *gv = nullptr;
+    TileSrc* srcs = nullptr;
+    std::uint32_t* cseg = nullptr;
+    HMXG_TRY(dev_upload(&gd, cds->dgen, plan.d_elems, d.comp));
+    HMXG_TRY(dev_upload(&gb, cds->bgen, plan.b_elems, d.comp));
+    HMXG_TRY(dev_upload(&gv, cds->vgen, plan.v_elems, d.comp));
+    HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
+    HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
+    if (plan.tile_elems) {
+      HMXG_CUDA(cudaMalloc(&d.tiles, plan.tile_elems * sizeof(double)));
+      const std::uint64_t nch = plan.chunk_seg.size();
+      tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
+                                                                                               d.tiles, nch);
+      HMXG_CUDA(cudaGetLastError());
+    }
+    HMXG_CUDA(cudaStreamSynchronize(d.comp));
+    cudaFree(gd);
+    cudaFree(gb);
+    cudaFree(gv);
+    cudaFree(srcs);
+    cudaFree(cseg);
     HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
     HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
-    HMXG_TRY(dev_upload(&d.perm, cds->perm, plan.n, d.comp));
-    HMXG_TRY(dev_upload(&d.iperm, iperm.data(), plan.n, d.comp));
+    HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
-    d.resident_bytes = 8 * (plan.d_elems + plan.b_elems + plan.v_elems) + sizeof(Task) * plan.tasks.size() +
-                       sizeof(Seg) * plan.segs.size() + 8 * plan.n;
+    d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
+                       4 * plan.ipmap.size();
   }
   *out = mat.release();
   return HMXG_OK;
@@ -385,7 +440,7 @@ int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   std::memset(out, 0, sizeof *out);
   if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
     out->kind = idx == 0 ? 0 : 4;
-    out->tiles = static_cast<std::uint32_t>((p.n + 255) / 256);
+    out->tiles = static_cast<std::uint32_t>((p.n + 31) / 32);
     out->io_bytes_per_col = 16.0 * p.n;
     out->gen_bytes = 4.0 * p.n;  // the permutation itself
   } else {

@@ -1,15 +1,21 @@
 // kernels.cuh — sm_100a kernels of the evaluator.
 //
-//  * grouped_gemm<TRANS_A>: one CTA per (output row tile, 64-column block); its K loop runs
-//    over the tile's segment list, so a whole far+downward sum or a whole leaf row
-//    (V_i S_i + sum_j D_ij Wp_j) is accumulated in registers and stored once.
-//    FP64 math on the tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; tcgen05 has no
-//    f64 kind). Operands are staged global->shared by a 3-stage cp.async ring
-//    with zero-fill for ragged M/K/N edges (two-means leaves of 15..256 points).
-//  * gather_rows / scatter_rows: the permutation into and out of tree order
-//    (executor.cpp:35-39, :245-254); coalesced along the output, the scattered side is a
-//    per-column gather that stays L2 resident.
+//  * tile_a: one-time (upload) re-layout of every GEMM A operand (V^T, V, B_ij, D_ij
+//    row tiles) into zero-padded, XOR-swizzled 64 x 16 FP64 chunks, so the main kernel
+//    streams A with one 8 KB bulk copy per chunk and reads it without bank conflicts.
+//  * grouped_gemm: warp-specialized, mbarrier-pipelined grouped FP64 GEMM. One CTA owns
+//    one (output row tile, 64-column block); its K loop walks the tile's segment list,
+//    so a whole far+downward sum or a whole leaf row (V_i S_i + sum_j D_ij Wp_j) is
+//    accumulated in registers and stored once (single writer, no atomics). A producer
+//    warp streams A chunks with cp.async.bulk and B tiles (rows of Wp/T/S, 16 x 64) with
+//    TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep ring; four consumer
+//    warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4 — tcgen05 has no f64 kind).
+//  * permute_in / permute_out: the permutation into and out of the padded tree order
+//    (executor.cpp:35-39, :245-254), fused with the transpose between the user's column-
+//    major W/Y and the point-major (Q-contiguous) internal buffers Wp/T/S/Yp.
 #pragma once
+
+#include <cuda.h>
 
 #include <cstdint>
 
@@ -17,123 +23,177 @@
 
 namespace hmxg {
 
-constexpr int kBM = 64;       // output rows per CTA tile
-constexpr int kBN = 64;       // output columns per CTA tile
-constexpr int kBK = 16;       // K chunk per pipeline stage
-constexpr int kStages = 3;
-constexpr int kThreads = 128; // 4 warps, 2 x 2 warp grid of 32 x 32 warp tiles
-constexpr int kAStrideN = kBM + 8;  // A stored [k][r] (non-transposed A)
-constexpr int kAStrideT = kBK + 4;  // A stored [r][k] (transposed A)
-constexpr int kBStride = kBK + 4;   // B stored [n][k]
-constexpr int kAStageElems = (kBK * kAStrideN > kBM * kAStrideT) ? kBK * kAStrideN : kBM * kAStrideT;
-constexpr int kBStageElems = kBN * kBStride;
-constexpr int kSmemBytes = kStages * (kAStageElems + kBStageElems) * 8;
+constexpr int kBM = 64;        // output rows per CTA tile
+constexpr int kBN = 64;        // output columns per CTA tile
+constexpr int kBK = 16;        // K rows per pipeline chunk
+#ifndef HMXG_STAGES
+#define HMXG_STAGES 4
+#endif
+constexpr int kStages = HMXG_STAGES;
+constexpr int kConsumerWarps = 4;  // 2 x 2 grid of 32 x 32 warp tiles
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kChunkElems = kBM * kBK;               // A chunk: 64 x 16 doubles
+constexpr int kChunkBytes = kChunkElems * 8;         // 8 KB
+// B tile: 16 rows (k) x kBPitch columns, row major as TMA writes it. The pitch of 68
+// doubles (544 B) shifts consecutive k rows by 8 banks, so a fragment load (4 k rows x 8
+// columns) hits every bank exactly twice: conflict-free without a swizzle pattern. The 4
+// extra columns are the next column block's (or TMA zero fill past Q).
+constexpr int kBPitch = kBN + 4;
+constexpr int kBTileBytes = kBPitch * kBK * 8;       // 8704 B
+constexpr int kStageBytes = kChunkBytes + kBTileBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + 1024;  // + barriers + align slack
 
-struct EvalParams {
-  const double* gen[3];        // D, B, V generator bases
-  double* buf[kNumBufs];       // Wp, T, S, Yp
-  std::uint64_t ld[kNumBufs];  // leading dimensions
-  const Task* tasks;           // first task of the phase
-  const Seg* segs;
+struct GemmParams {
+  const double* tiles;          // pre-tiled A chunks
+  const Task* tasks;            // first task of the phase
+  const SegDev* segs;
+  double* buf[kNumBufs];        // Wp, T, S, Yp
+  std::uint64_t ld[kNumBufs];
   std::uint32_t q;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int bytes = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      "@!done bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_g2s(void* dst, const CUtensorMap* map, int x, int y, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ double lds64(std::uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
 
-// Uniform selects instead of dynamic indexing into the parameter arrays (which would
-// copy them to local memory).
-__device__ __forceinline__ const double* pick_gen(const EvalParams& p, unsigned g) {
-  return g == kGenD ? p.gen[kGenD] : (g == kGenB ? p.gen[kGenB] : p.gen[kGenV]);
-}
-__device__ __forceinline__ double* pick_buf(const EvalParams& p, unsigned b) {
+// Uniform selects instead of dynamic indexing into parameter arrays (no local copies).
+__device__ __forceinline__ double* pick_buf(const GemmParams& p, unsigned b) {
   return b == kBufWp ? p.buf[kBufWp] : (b == kBufT ? p.buf[kBufT] : (b == kBufS ? p.buf[kBufS] : p.buf[kBufYp]));
 }
-__device__ __forceinline__ std::uint64_t pick_ld(const EvalParams& p, unsigned b) {
+__device__ __forceinline__ std::uint64_t pick_ld(const GemmParams& p, unsigned b) {
   return b == kBufWp ? p.ld[kBufWp] : (b == kBufT ? p.ld[kBufT] : (b == kBufS ? p.ld[kBufS] : p.ld[kBufYp]));
 }
 
-template <bool TRANS_A>
-__global__ void __launch_bounds__(kThreads) grouped_gemm(EvalParams p) {
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;                                // kStages * kAStageElems
-  double* Bs = smem + kStages * kAStageElems;       // kStages * kBStageElems
+// A chunk layout: element (k, r) of a 64 x 16 chunk lives at k*64 + (r ^ ((k & 3) << 3)).
+// The XOR spreads the four k rows a fragment load touches over both bank halves.
+__host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 3)); }
 
-  const Task task = p.tasks[blockIdx.x];
-  const std::uint32_t c0 = blockIdx.y * kBN;
-  const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
-  const int m = task.m;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-
-  // number of K chunks over all segments
-  int nchunks = 0;
-  for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s)
-    nchunks += (p.segs[s].k + kBK - 1) / kBK;
-
-  // loader cursor
-  std::uint32_t ls = task.seg_begin;
-  std::uint32_t lk = 0;
-  auto load_stage = [&](int stage) {
-    if (ls < task.seg_end) {
-      const Seg sg = p.segs[ls];
-      const double* a = pick_gen(p, sg.gen) + sg.a_off;
-      const std::uint64_t ldb = pick_ld(p, sg.bbuf);
-      const double* b = pick_buf(p, sg.bbuf) + sg.b_row + static_cast<std::uint64_t>(c0) * ldb;
-      const int kr = min(kBK, static_cast<int>(sg.k - lk));
-      double* as = As + stage * kAStageElems;
-      double* bs = Bs + stage * kBStageElems;
-      if (TRANS_A) {
-        // A(r,k) = a[k + r*lda]; contiguous along k -> store [r][k]
-        const int k = tid % kBK;
-#pragma unroll
-        for (int j = 0; j < (kBM * kBK) / kThreads; ++j) {
-          const int r = tid / kBK + j * (kThreads / kBK);
-          const bool ok = r < m && k < kr;
-          cp_async8(as + r * kAStrideT + k, ok ? a + (lk + k) + static_cast<std::uint64_t>(r) * sg.lda : a, ok);
-        }
-      } else {
-        // A(r,k) = a[r + k*lda]; contiguous along r -> store [k][r]
-        const int r = tid % kBM;
-#pragma unroll
-        for (int j = 0; j < (kBM * kBK) / kThreads; ++j) {
-          const int k = tid / kBM + j * (kThreads / kBM);
-          const bool ok = r < m && k < kr;
-          cp_async8(as + k * kAStrideN + r, ok ? a + r + static_cast<std::uint64_t>(lk + k) * sg.lda : a, ok);
-        }
+// ---------------------------------------------------------------- A pre-tiling
+__global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
+                       const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,
+                       double* __restrict__ tiles, std::uint64_t nchunks) {
+  for (std::uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const TileSrc s = srcs[chunk_seg[c]];
+    const std::uint64_t chunk_in_seg = (c * kChunkElems - s.tile_off) / kChunkElems;
+    const double* a = (s.gen == kGenD ? gd : (s.gen == kGenB ? gb : gv)) + s.a_off;
+    double* out = tiles + c * kChunkElems;
+    for (int e = threadIdx.x; e < kChunkElems; e += blockDim.x) {
+      int k, r;
+      if (s.trans) {  // A(r,k) = a[k + r*lda]: let consecutive threads walk k
+        k = e % kBK;
+        r = e / kBK;
+      } else {        // A(r,k) = a[r + k*lda]: consecutive threads walk r
+        r = e % kBM;
+        k = e / kBM;
       }
-      {
-        const int k = tid % kBK;
-#pragma unroll
-        for (int j = 0; j < (kBN * kBK) / kThreads; ++j) {
-          const int n = tid / kBK + j * (kThreads / kBK);
-          const bool ok = k < kr && n < static_cast<int>(ncols);
-          cp_async8(bs + n * kBStride + k, ok ? b + (lk + k) + static_cast<std::uint64_t>(n) * ldb : b, ok);
+      const std::uint64_t kk = chunk_in_seg * kBK + k;
+      double v = 0.0;
+      if (r < s.m && kk < s.k)
+        v = s.trans ? a[kk + static_cast<std::uint64_t>(r) * s.lda] : a[r + kk * s.lda];
+      out[a_swz(k, r)] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- grouped GEMM
+__global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
+grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
+             const __grid_constant__ CUtensorMap tm_s, const GemmParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                         ~std::uintptr_t(1023));
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * kStageBytes);
+  std::uint64_t* empty = full + kStages;
+
+  // column-block-fastest raster: the CTAs of one row tile run back to back, so its A
+  // chunks are fetched from HBM once and re-served from L2 to every column block
+  const std::uint32_t col_blocks = (p.q + kBN - 1) / kBN;
+  const Task task = p.tasks[blockIdx.x / col_blocks];
+  const std::uint32_t c0 = (blockIdx.x % col_blocks) * kBN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: one elected lane streams the chunk sequence
+    if (lane == 0) {
+      std::uint32_t it = 0;
+      for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
+        const SegDev sg = p.segs[si];
+        const CUtensorMap* map = sg.bbuf == kBufWp ? &tm_wp : (sg.bbuf == kBufT ? &tm_t : &tm_s);
+        for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
+          const int stage = it % kStages;
+          if (it >= kStages) mbar_wait(&empty[stage], ((it / kStages) - 1) & 1);
+          unsigned char* st = smem + stage * kStageBytes;
+          mbar_expect_tx(&full[stage], kStageBytes);
+          bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
+                   &full[stage]);
+          // coordinates: {column (inner, Q-contiguous), row}
+          tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
+                     &full[stage]);
         }
-      }
-      lk += kBK;
-      if (lk >= sg.k) {
-        ++ls;
-        lk = 0;
       }
     }
-    cp_async_commit();
-  };
+    return;
+  }
+
+  // ---------------- consumers: 2 x 2 warps of 32 x 32
+  const int wm = warp & 1, wn = warp >> 1;
+  std::uint32_t nchunks = 0;
+  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
 
   double acc[4][4][2];
 #pragma unroll
@@ -141,76 +201,118 @@ __global__ void __launch_bounds__(kThreads) grouped_gemm(EvalParams p) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  const int fr = lane >> 2, fk = lane & 3;
+  // Warp-uniform trim of 8-row / 8-column fragments outside the task's valid rows and
+  // the last column block: their DMMAs are skipped, so a ragged tile (srank 46 in a
+  // 64-row tile) hands its tensor-pipe cycles to the other CTA on the SM.
+  const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
+  const int live_i = min(4, max(0, (static_cast<int>(task.m) - wm * 32 + 7) / 8));
+  const int live_j = min(4, max(0, (static_cast<int>(ncols) - wn * 32 + 7) / 8));
+  // Fragment addresses (shared window, bytes) relative to the stage base. A: swizzled
+  // 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile.
+  std::uint32_t a_off[4][4], b_off[4][4];  // [k step][fragment]
 #pragma unroll
-  for (int st = 0; st < kStages - 1; ++st) load_stage(st);
-
-  for (int it = 0; it < nchunks; ++it) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k = ks * 4 + fk;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a_off[ks][i] = 8u * a_swz(k, wm * 32 + i * 8 + fr);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = wn * 32 + j * 8 + fr;
+      b_off[ks][j] = kChunkBytes + (k * kBPitch + n) * 8;
+    }
+  }
+  const std::uint32_t smem_base = smem_u32(smem);
+  for (std::uint32_t it = 0; it < nchunks; ++it) {
     const int stage = it % kStages;
-    const double* as = As + stage * kAStageElems;
-    const double* bs = Bs + stage * kBStageElems;
+    mbar_wait(&full[stage], (it / kStages) & 1);
+    const std::uint32_t st = smem_base + stage * kStageBytes;
+    // register double buffer: fragments of k step ks+1 load while step ks multiplies
+    double af[2][4], bf[2][4];
 #pragma unroll
-    for (int kk = 0; kk < kBK; kk += 4) {
-      double af[4], bf[4];
+    for (int i = 0; i < 4; ++i) af[0][i] = lds64(st + a_off[0][i]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = wm * 32 + i * 8 + (lane >> 2);
-        const int k = kk + (lane & 3);
-        af[i] = TRANS_A ? as[r * kAStrideT + k] : as[k * kAStrideN + r];
-      }
+    for (int j = 0; j < 4; ++j) bf[0][j] = lds64(st + b_off[0][j]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int n = wn * 32 + j * 8 + (lane >> 2);
-        bf[j] = bs[n * kBStride + kk + (lane & 3)];
+    for (int ks = 0; ks < 4; ++ks) {
+      const int cur = ks & 1;
+      if (ks + 1 < 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[cur ^ 1][i] = lds64(st + a_off[ks + 1][i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[cur ^ 1][j] = lds64(st + b_off[ks + 1][j]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < 4; ++j)
+          if (i < live_i && j < live_j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
     }
-    load_stage((it + kStages - 1) % kStages);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
   }
-  cp_async_wait<0>();
 
-  // epilogue: every element of the tile is stored exactly once (zeros for empty tasks)
+  // epilogue: every valid element of the tile is stored exactly once (zeros for empty tasks)
   double* C = pick_buf(p, task.cbuf);
   const std::uint64_t ldc = pick_ld(p, task.cbuf);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int row = wm * 32 + i * 8 + (lane >> 2);
-    if (row >= m) continue;
+    const int row = wm * 32 + i * 8 + fr;
+    if (row >= task.m) continue;
+    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int col = wn * 32 + j * 8 + 2 * (lane & 3);
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (col + e < static_cast<int>(ncols))
-          C[task.c_row + row + static_cast<std::uint64_t>(c0 + col + e) * ldc] = acc[i][j][e];
+      const int col = wn * 32 + j * 8 + 2 * fk;
+      if (col + 1 < static_cast<int>(ncols))
+        *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      else if (col < static_cast<int>(ncols))
+        crow[col] = acc[i][j][0];
     }
   }
 }
 
-// Wp[pos, c] = W[perm[pos], c]
-__global__ void gather_rows(const double* __restrict__ w, std::uint64_t ldw,
-                            const std::uint32_t* __restrict__ perm, double* __restrict__ wp,
-                            std::uint64_t ldwp, std::uint32_t n, std::uint32_t q) {
-  const std::uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= n) return;
-  const std::uint32_t src = perm[pos];
-  for (std::uint32_t c = blockIdx.y; c < q; c += gridDim.y)
-    wp[pos + c * ldwp] = w[src + c * ldw];
+// Transpose-permute into the point-major internal layout: Wp[ipmap[r], c] = W[r, c].
+// A 32 x 32 tile is read column by column (256 B contiguous per column of W), turned
+// around in shared memory and written row by row (256 B contiguous per point row of Wp),
+// so both sides move whole cache lines although the rows land in permuted order.
+constexpr int kTT = 32;
+__global__ void __launch_bounds__(256) permute_in(const double* __restrict__ w, std::uint64_t ldw,
+                                                  const std::uint32_t* __restrict__ ipmap, double* __restrict__ wp,
+                                                  std::uint64_t ldwp, std::uint32_t n, std::uint32_t q) {
+  __shared__ double tile[kTT][kTT + 1];
+  const std::uint32_t r0 = blockIdx.x * kTT, c0 = blockIdx.y * kTT;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const std::uint32_t r = r0 + tx, c = c0 + ty + k;
+    tile[ty + k][tx] = (r < n && c < q) ? __ldg(w + r + static_cast<std::uint64_t>(c) * ldw) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const std::uint32_t r = r0 + ty + k, c = c0 + tx;
+    if (r < n && c < q) wp[static_cast<std::uint64_t>(ipmap[r]) * ldwp + c] = tile[tx][ty + k];
+  }
 }
 
-// Y[r, c] = Yp[iperm[r], c]  (== Y[perm[pos], c] = Yp[pos, c])
-__global__ void scatter_rows(const double* __restrict__ yp, std::uint64_t ldyp,
-                             const std::uint32_t* __restrict__ iperm, double* __restrict__ y,
-                             std::uint64_t ldy, std::uint32_t n, std::uint32_t q) {
-  const std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const std::uint32_t src = iperm[r];
-  for (std::uint32_t c = blockIdx.y; c < q; c += gridDim.y)
-    y[r + c * ldy] = yp[src + c * ldyp];
+// Inverse: Y[r, c] = Yp[ipmap[r], c] (point rows read whole, columns of Y written whole).
+__global__ void __launch_bounds__(256) permute_out(const double* __restrict__ yp, std::uint64_t ldyp,
+                                                   const std::uint32_t* __restrict__ ipmap, double* __restrict__ y,
+                                                   std::uint64_t ldy, std::uint32_t n, std::uint32_t q) {
+  __shared__ double tile[kTT][kTT + 1];
+  const std::uint32_t r0 = blockIdx.x * kTT, c0 = blockIdx.y * kTT;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const std::uint32_t r = r0 + ty + k, c = c0 + tx;
+    tile[ty + k][tx] = (r < n && c < q) ? __ldg(yp + static_cast<std::uint64_t>(ipmap[r]) * ldyp + c) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const std::uint32_t r = r0 + tx, c = c0 + ty + k;
+    if (r < n && c < q) y[r + static_cast<std::uint64_t>(c) * ldy] = tile[tx][ty + k];
+  }
 }
 
 }  // namespace hmxg

@@ -124,22 +124,38 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   if (std::max({plan.d_elems, plan.b_elems, plan.v_elems}) >= (std::uint64_t(1) << 62))
     return fail(err, "cds: generator arrays too large");
 
-  // --- T/S rows: siblings adjacent so [T_lc; T_rc] is one contiguous operand
+  // --- padded row layouts: leaves in Wp/Yp, active nodes in T/S, 16-row aligned blocks
+  auto pad16 = [](std::uint64_t r) { return (r + kRowAlign - 1) / kRowAlign * kRowAlign; };
+  plan.leaf_row.assign(nn, 0);
+  std::vector<std::uint32_t> leaves_by_start;
+  for (std::uint32_t i = 0; i < nn; ++i)
+    if (is_leaf(i)) leaves_by_start.push_back(i);
+  std::sort(leaves_by_start.begin(), leaves_by_start.end(),
+            [&](std::uint32_t a, std::uint32_t b) { return v.start[a] < v.start[b]; });
+  std::uint64_t prow = 0;
+  for (std::uint32_t i : leaves_by_start) {
+    plan.leaf_row[i] = prow;
+    prow += pad16(size_of(i));
+  }
+  if (prow > std::numeric_limits<std::uint32_t>::max() - kRowAlign) return fail(err, "cds: too many points");
+  plan.rows_pad = prow;
+  plan.pmap.assign(prow, 0xffffffffu);
+  plan.ipmap.assign(v.n, 0);
+  for (std::uint32_t i : leaves_by_start)
+    for (std::uint32_t r = 0; r < size_of(i); ++r) {
+      const std::uint32_t orig = v.perm[v.start[i] + r];
+      plan.pmap[plan.leaf_row[i] + r] = orig;
+      plan.ipmap[orig] = static_cast<std::uint32_t>(plan.leaf_row[i] + r);
+    }
   plan.node_off.assign(nn, 0);
   std::uint64_t rows = 0;
-  if (active(0)) {
-    plan.node_off[0] = rows;
-    rows += v.sranks[0];
-  }
-  for (std::uint32_t i : order) {
-    if (is_leaf(i)) continue;
-    for (std::uint32_t c : {v.lchild[i], v.rchild[i]}) {
-      plan.node_off[c] = rows;
-      if (active(c)) rows += v.sranks[c];
+  for (std::uint32_t i : order)
+    if (active(i)) {
+      plan.node_off[i] = rows;
+      rows += pad16(v.sranks[i]);
     }
-  }
-  if (rows > std::numeric_limits<std::uint32_t>::max()) return fail(err, "cds: too many skeleton rows");
-  plan.skel_rows = rows;
+  if (rows > std::numeric_limits<std::uint32_t>::max() - kRowAlign) return fail(err, "cds: too many skeleton rows");
+  plan.skel_rows = std::max<std::uint64_t>(rows, kRowAlign);
 
   const std::uint32_t bm = tile_m;
   auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs, Phase& ph) {
@@ -151,27 +167,40 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       task.cbuf = cbuf;
       task.m = static_cast<std::uint16_t>(std::min(bm, m - r0));
       task.seg_begin = static_cast<std::uint32_t>(plan.segs.size());
-      emit_segs(r0);
+      emit_segs(r0, task.m);
       task.seg_end = static_cast<std::uint32_t>(plan.segs.size());
       for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s) {
-        ph.flops_per_col += 2.0 * task.m * plan.segs[s].k;
-        ph.gen_bytes += 8.0 * task.m * plan.segs[s].k;
-        if (t == 0) ph.io_bytes_per_col += 8.0 * plan.segs[s].k;  // B rows, read once per node
+        const double k = plan.tile_src[s].k;
+        ph.flops_per_col += 2.0 * task.m * k;
+        ph.gen_bytes += 8.0 * task.m * k;
+        if (t == 0) ph.io_bytes_per_col += 8.0 * k;  // B rows, read once per node
       }
       plan.tasks.push_back(task);
     }
     ph.io_bytes_per_col += 8.0 * m;  // C rows, written once
     plan.max_m = std::max(plan.max_m, m);
   };
-  auto push_seg = [&](Gen gen, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k, Buf bbuf,
-                      std::uint64_t b_row) {
+  // A operand rows [r0, r0+m) of the generator block at a_off; K columns; B rows b_row.
+  auto push_seg = [&](Gen gen, bool trans, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k,
+                      std::uint32_t m, Buf bbuf, std::uint64_t b_row) {
     if (k == 0) return;
-    plan.segs.push_back(Seg{a_off, static_cast<std::uint32_t>(lda), static_cast<std::uint32_t>(k),
-                            static_cast<std::uint32_t>(b_row), static_cast<std::uint16_t>(gen),
-                            static_cast<std::uint16_t>(bbuf)});
+    const std::uint64_t chunks = (k + kRowAlign - 1) / kRowAlign;
+    TileSrc ts{};
+    ts.a_off = a_off;
+    ts.tile_off = plan.tile_elems;
+    ts.lda = static_cast<std::uint32_t>(lda);
+    ts.k = static_cast<std::uint32_t>(k);
+    ts.m = static_cast<std::uint16_t>(m);
+    ts.gen = gen;
+    ts.trans = trans ? 1 : 0;
+    for (std::uint64_t c = 0; c < chunks; ++c) plan.chunk_seg.push_back(static_cast<std::uint32_t>(plan.segs.size()));
+    plan.segs.push_back(SegDev{plan.tile_elems, static_cast<std::uint32_t>(b_row),
+                               static_cast<std::uint16_t>(chunks), static_cast<std::uint16_t>(bbuf)});
+    plan.tile_src.push_back(ts);
+    plan.tile_elems += chunks * kRowAlign * bm;
   };
-  auto open_phase = [&](PhaseKind kind, bool trans, std::uint32_t level) {
-    plan.phases.push_back(Phase{kind, trans, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0, 0.0, 0.0});
+  auto open_phase = [&](PhaseKind kind, std::uint32_t level) {
+    plan.phases.push_back(Phase{kind, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0, 0.0, 0.0});
   };
   auto close_phase = [&]() {
     Phase& ph = plan.phases.back();
@@ -183,16 +212,21 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   std::uint32_t max_h = 0;
   for (std::uint32_t i = 0; i < nn; ++i) max_h = std::max(max_h, sub_h[i]);
   for (std::uint32_t h = 0; h <= max_h; ++h) {
-    open_phase(kPhaseUp, true, h);
+    open_phase(kPhaseUp, h);
     for (std::uint32_t i : order) {
       if (sub_h[i] != h || !active(i)) continue;
       const std::uint64_t lda = v_width(i);
       const std::uint64_t vo = v.vptr[vslot[i]];
-      add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0) {
-        if (is_leaf(i))
-          push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufWp, v.start[i]);
-        else
-          push_seg(kGenV, vo + std::uint64_t(r0) * lda, lda, lda, kBufT, plan.node_off[v.lchild[i]]);
+      add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
+        if (is_leaf(i)) {
+          push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, lda, m, kBufWp, plan.leaf_row[i]);
+        } else {
+          const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
+          const std::uint64_t srl = v.sranks[lc];
+          if (active(lc)) push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc]);
+          if (active(rc))
+            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT, plan.node_off[rc]);
+        }
       }, plan.phases.back());
     }
     close_phase();
@@ -201,18 +235,18 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   // --- downward with the far pass folded in, by depth:
   //     S_c = sum_{far (c,j)} B_cj T_j + V_p[rows of c] S_p
   for (std::uint32_t d = 0; d <= height; ++d) {
-    open_phase(kPhaseDown, false, d);
+    open_phase(kPhaseDown, d);
     for (std::uint32_t c : order) {
       if (v.level[c] != d || !active(c)) continue;
       const std::uint32_t p = v.parent[c];
-      add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0) {
+      add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0, std::uint32_t m) {
         for (std::uint64_t s : far_of[c]) {
           const std::uint32_t j = v.far_pairs[2 * s + 1];
-          push_seg(kGenB, v.bptr[s] + r0, v.sranks[c], v.sranks[j], kBufT, plan.node_off[j]);
+          push_seg(kGenB, false, v.bptr[s] + r0, v.sranks[c], v.sranks[j], m, kBufT, plan.node_off[j]);
         }
         if (p != HMXG_NO_NODE && active(p)) {
           const std::uint64_t row_in_parent = (c == v.lchild[p]) ? 0 : v.sranks[v.lchild[p]];
-          push_seg(kGenV, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], kBufS,
+          push_seg(kGenV, false, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], m, kBufS,
                    plan.node_off[p]);
         }
       }, plan.phases.back());
@@ -221,15 +255,15 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   }
 
   // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j (every leaf row written once)
-  open_phase(kPhaseLeaf, false, 0);
+  open_phase(kPhaseLeaf, 0);
   for (std::uint32_t i : order) {
     if (!is_leaf(i)) continue;
     const std::uint32_t m = size_of(i);
-    add_tiles(m, kBufYp, v.start[i], [&](std::uint32_t r0) {
-      if (active(i)) push_seg(kGenV, v.vptr[vslot[i]] + r0, m, v.sranks[i], kBufS, plan.node_off[i]);
+    add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
+      if (active(i)) push_seg(kGenV, false, v.vptr[vslot[i]] + r0, m, v.sranks[i], mt, kBufS, plan.node_off[i]);
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
-        push_seg(kGenD, v.dptr[s] + r0, m, size_of(j), kBufWp, v.start[j]);
+        push_seg(kGenD, false, v.dptr[s] + r0, m, size_of(j), mt, kBufWp, plan.leaf_row[j]);
       }
     }, plan.phases.back());
   }

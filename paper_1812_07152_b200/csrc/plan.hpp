@@ -6,16 +6,20 @@
 // whose tasks are output row tiles with a list of K segments:
 //
 //   gather    Wp = W[perm, :]                                   (executor.cpp:35-39)
-//   up-leaf   T_i = V_i^T Wp_i                 one launch        (executor.cpp:56-61)
-//   up-h      T_i = V_i^T [T_lc; T_rc]         one per height    (executor.cpp:62-71)
+//   up-leaf   T_i = V_i^T Wp_i                  one launch       (executor.cpp:56-61)
+//   up-h      T_i = V_i^T [T_lc; T_rc]          one per height   (executor.cpp:62-71)
 //   down-d    S_c = sum_j B_cj T_j + V_p[c] S_p one per depth    (executor.cpp:105-110, 85-102)
-//   leaf      Y'_i = V_i S_i + sum_j D_ij Wp_j one launch        (executor.cpp:79-84, 112-117)
+//   leaf      Y'_i = V_i S_i + sum_j D_ij Wp_j  one launch       (executor.cpp:79-84, 112-117)
 //   scatter   Y[perm, :] = Y'                                    (executor.cpp:245-254)
 //
 // The far pass is folded into the downward pass (far terms only need T, which is complete
 // after the upward pass), and the leaf downward term is folded into the near pass, so every
 // output tile is written exactly once by one CTA: no atomics, no memset, no read-modify-
 // write of S (the reference's single-writer invariant, executor.hpp:48-50).
+//
+// Device layout: every node's row block in Wp / Yp (leaves) and T / S (active nodes) starts
+// on a 16-row boundary and is zero-padded to a multiple of 16 rows, so each 16-row B chunk
+// the TMA engine fetches lies inside one node block (no foreign rows enter a sum).
 #pragma once
 
 #include <cstdint>
@@ -26,24 +30,37 @@
 
 namespace hmxg {
 
+constexpr std::uint32_t kRowAlign = 16;  // = the kernel's K chunk
+
 // Operand buffers a task can read (B side) or write (C side).
 enum Buf : std::uint16_t { kBufWp = 0, kBufT = 1, kBufS = 2, kBufYp = 3, kNumBufs = 4 };
-// Generator arrays a segment's A operand lives in.
-enum Gen : std::uint16_t { kGenD = 0, kGenB = 1, kGenV = 2 };
+// Generator arrays an A operand is tiled from.
+enum Gen : std::uint8_t { kGenD = 0, kGenB = 1, kGenV = 2 };
 
-// One K segment of a task: C_tile += A_seg(tile rows, 0:k) * B_seg(0:k, cols).
-// A is column major with leading dimension lda; with `trans` the stored matrix is A^T
-// (A(r,k) = a[k + r*lda]). a_off is the element offset (tile row already applied) into
-// generator array `gen`; b_row is the first row of the B operand inside buffer `bbuf`.
-struct Seg {
+// Source of one pre-tiled A operand: rows [0, m) of the tile, K columns, from generator
+// `gen` at element offset a_off, column major with leading dimension lda; with `trans`
+// the stored matrix is A^T (A(r,k) = a[k + r*lda]). Tiled to tile_off (in doubles).
+struct TileSrc {
   std::uint64_t a_off;
+  std::uint64_t tile_off;
   std::uint32_t lda;
   std::uint32_t k;
+  std::uint16_t m;
+  std::uint8_t gen;
+  std::uint8_t trans;
+  std::uint32_t pad;
+};
+static_assert(sizeof(TileSrc) == 32, "TileSrc layout");
+
+// One K segment of a task as the GEMM kernel sees it: nchunks pre-tiled A chunks at
+// tile_off, and B rows [b_row, b_row + 16*nchunks) of buffer bbuf.
+struct SegDev {
+  std::uint64_t tile_off;
   std::uint32_t b_row;
-  std::uint16_t gen;
+  std::uint16_t nchunks;
   std::uint16_t bbuf;
 };
-static_assert(sizeof(Seg) == 24, "Seg layout");
+static_assert(sizeof(SegDev) == 16, "SegDev layout");
 
 // One output row tile: rows [c_row, c_row + m) of buffer cbuf, all columns (grid.y).
 struct Task {
@@ -59,21 +76,27 @@ enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2 };
 
 struct Phase {
   PhaseKind kind;
-  bool trans_a;          // upward phases read V^T
   std::uint32_t task_begin, task_end;
-  std::uint32_t level;   // height (up) or depth (down)
-  double flops_per_col;  // 2*sum(m*k) over the phase's tiles, algorithmic
-  double gen_bytes;      // generator (A operand) bytes the phase reads once per evaluation
+  std::uint32_t level;      // height (up) or depth (down)
+  double flops_per_col;     // 2*sum(m*k) over the phase's tiles, algorithmic
+  double gen_bytes;         // generator (A operand) bytes the phase reads once per evaluation
   double io_bytes_per_col;  // B operand rows read + C rows written, once per node, per column
 };
 
 struct Plan {
   std::uint64_t n = 0;
   std::uint32_t num_nodes = 0;
-  std::uint64_t skel_rows = 0;  // rows of T and S
+  std::uint64_t rows_pad = 0;           // rows of Wp / Yp (padded tree order)
+  std::uint64_t skel_rows = 0;          // rows of T and S (padded)
+  std::vector<std::uint32_t> pmap;      // padded row -> original point, 0xffffffff for pad
+  std::vector<std::uint32_t> ipmap;     // original point -> padded row
+  std::vector<std::uint64_t> leaf_row;  // padded Wp/Yp row of each leaf
   std::vector<std::uint64_t> node_off;  // T/S row of each active node
   std::vector<Task> tasks;
-  std::vector<Seg> segs;
+  std::vector<SegDev> segs;
+  std::vector<TileSrc> tile_src;        // one per segment (same order as segs)
+  std::vector<std::uint32_t> chunk_seg; // pre-tiled chunk -> segment
+  std::uint64_t tile_elems = 0;
   std::vector<Phase> phases;
   std::uint64_t d_elems = 0, b_elems = 0, v_elems = 0;
   std::uint32_t max_m = 0;
