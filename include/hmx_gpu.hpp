@@ -1,0 +1,147 @@
+// hmx_gpu.hpp — drop-in replacement of hmx::evaluate for reference (hmx) callers.
+//
+// Header-only C++ shim over the C-ABI of include/hmxg.h. A maintainer of the reference
+// switches a call site from
+//     hmx::DenseMatrix y = hmx::evaluate(cds, plan, w, &stats);
+// (/root/reference/proj/include/hmx/executor.hpp:51-54) to
+//     hmx::DenseMatrix y = hmx_gpu::evaluate(cds, plan, w, &stats);
+// with identical semantics:
+//   * w.rows != cds.tree.num_points()  -> std::invalid_argument (executor.cpp:277-278)
+//   * w.cols == 0                      -> n x 0 result          (executor.cpp:279-282)
+//   * stats->locked_pairs == 0, stats->seconds = wall time     (executor.cpp:289-294)
+//   * the plan's lowering switches are accepted and ignored (they only pick a CPU
+//     schedule; every schedule gives the same Y, executor.hpp:48-50)
+// Other C-ABI failures map to std::runtime_error (status 2/3/4: CUDA, memory, collective).
+// Requires the reference headers on the include path (hmx/executor.hpp) and linking
+// against libhmxg.so.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hmx/executor.hpp"
+#include "hmxg.h"
+
+namespace hmx_gpu {
+
+[[noreturn]] inline void raise(int status) {
+  const std::string msg = hmxg_last_error();
+  if (status == HMXG_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error("hmxg status " + std::to_string(status) + ": " + msg);
+}
+
+inline void check(int status) {
+  if (status != HMXG_OK) raise(status);
+}
+
+// Flattened pair lists kept alive next to the view they back.
+struct CdsView {
+  hmxg_cds_view view{};
+  std::vector<std::uint32_t> near_flat, far_flat;
+
+  explicit CdsView(const hmx::CDS& cds) {
+    const auto& t = cds.tree;
+    for (const auto& [i, j] : cds.near_order) near_flat.insert(near_flat.end(), {i, j});
+    for (const auto& [i, j] : cds.far_order) far_flat.insert(far_flat.end(), {i, j});
+    view.n = t.num_points();
+    view.num_nodes = t.num_nodes;
+    view.height = t.height;
+    view.parent = t.parent.data();
+    view.lchild = t.lchild.data();
+    view.rchild = t.rchild.data();
+    view.start = t.start.data();
+    view.end = t.end.data();
+    view.level = t.level.data();
+    view.perm = t.perm.data();
+    view.sranks = cds.sranks.data();
+    view.participating = cds.participating.data();
+    view.num_near = cds.near_order.size();
+    view.near_pairs = near_flat.data();
+    view.num_far = cds.far_order.size();
+    view.far_pairs = far_flat.data();
+    view.num_v = cds.v_order.size();
+    view.v_order = cds.v_order.data();
+    view.dptr = cds.dptr.data();
+    view.bptr = cds.bptr.data();
+    view.vptr = cds.vptr.data();
+    view.dgen = cds.dgen.data();
+    view.bgen = cds.bgen.data();
+    view.vgen = cds.vgen.data();
+  }
+};
+
+// A CDS resident on one or more GPUs (column shards over `devices`).
+class Evaluator {
+ public:
+  explicit Evaluator(const hmx::CDS& cds, const std::vector<int>& devices = {0}) : n_(cds.tree.num_points()) {
+    check(hmxg_create(devices.data(), static_cast<int>(devices.size()), &ctx_));
+    CdsView v(cds);
+    const int rc = hmxg_upload(ctx_, &v.view, &mat_);
+    if (rc != HMXG_OK) {
+      hmxg_destroy(ctx_);
+      raise(rc);
+    }
+  }
+  Evaluator(const Evaluator&) = delete;
+  Evaluator& operator=(const Evaluator&) = delete;
+  ~Evaluator() {
+    hmxg_free(mat_);
+    hmxg_destroy(ctx_);
+  }
+
+  hmx::DenseMatrix evaluate(const hmx::DenseMatrix& w, hmx::EvalStats* stats = nullptr) const {
+    if (w.rows != n_) throw std::invalid_argument("evaluate: W row count does not match the point count");
+    hmx::DenseMatrix y(w.rows, w.cols);
+    hmxg_stats st{};
+    if (w.cols) check(hmxg_evaluate(mat_, w.data.data(), w.rows, w.cols, w.rows, y.data.data(), y.rows, 0, nullptr, &st));
+    if (stats) {
+      stats->locked_pairs = 0;
+      stats->seconds = st.seconds;
+    }
+    return y;
+  }
+
+ private:
+  std::size_t n_ = 0;
+  hmxg_ctx* ctx_ = nullptr;
+  hmxg_mat* mat_ = nullptr;
+};
+
+// hmx::evaluate(cds, plan, w, stats) on the GPU. The most recently used CDS stays
+// resident (keyed on object identity and generator storage), so repeated calls on the
+// same CDS upload it once.
+inline hmx::DenseMatrix evaluate(const hmx::CDS& cds, const hmx::EvalPlan& /*plan*/, const hmx::DenseMatrix& w,
+                                 hmx::EvalStats* stats = nullptr) {
+  if (w.rows != cds.tree.num_points())
+    throw std::invalid_argument("evaluate: W row count does not match the point count");
+  if (w.cols == 0) {
+    if (stats) *stats = {0, 0.0};
+    return hmx::DenseMatrix(w.rows, 0);
+  }
+  struct Cached {
+    const hmx::CDS* cds = nullptr;
+    const double* dgen = nullptr;
+    const double* vgen = nullptr;
+    std::size_t sizes = 0;
+    std::unique_ptr<Evaluator> ev;
+  };
+  static std::mutex mu;
+  static Cached cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const std::size_t sizes = cds.dgen.size() * 31 + cds.bgen.size() * 17 + cds.vgen.size();
+  if (cache.cds != &cds || cache.dgen != cds.dgen.data() || cache.vgen != cds.vgen.data() || cache.sizes != sizes) {
+    cache.ev.reset();
+    cache.ev = std::make_unique<Evaluator>(cds);
+    cache.cds = &cds;
+    cache.dgen = cds.dgen.data();
+    cache.vgen = cds.vgen.data();
+    cache.sizes = sizes;
+  }
+  return cache.ev->evaluate(w, stats);
+}
+
+}  // namespace hmx_gpu

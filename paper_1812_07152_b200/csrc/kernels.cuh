@@ -30,14 +30,14 @@ constexpr int kBK = 16;        // K rows per pipeline chunk
 #define HMXG_STAGES 4
 #endif
 constexpr int kStages = HMXG_STAGES;
-constexpr int kConsumerWarps = 4;  // 2 x 2 grid of 32 x 32 warp tiles
+constexpr int kConsumerWarps = 4;  // 2 x 2 warps, each 4 x 4 interleaved 8 x 8 fragments
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kChunkElems = kBM * kBK;               // A chunk: 64 x 16 doubles
 constexpr int kChunkBytes = kChunkElems * 8;         // 8 KB
 // B tile: 16 rows (k) x kBPitch columns, row major as TMA writes it. The pitch of 68
-// doubles (544 B) shifts consecutive k rows by 8 banks, so a fragment load (4 k rows x 8
-// columns) hits every bank exactly twice: conflict-free without a swizzle pattern. The 4
-// extra columns are the next column block's (or TMA zero fill past Q).
+// doubles (544 B) shifts consecutive k rows by 8 banks, so each half-warp of a fragment
+// load (4 k rows x 4 columns) covers all 32 banks once: conflict-free without a swizzle
+// pattern. The 4 extra columns are the next column block's (or TMA zero fill past Q).
 constexpr int kBPitch = kBN + 4;
 constexpr int kBTileBytes = kBPitch * kBK * 8;       // 8704 B
 constexpr int kStageBytes = kChunkBytes + kBTileBytes;
@@ -110,9 +110,11 @@ __device__ __forceinline__ std::uint64_t pick_ld(const GemmParams& p, unsigned b
   return b == kBufWp ? p.ld[kBufWp] : (b == kBufT ? p.ld[kBufT] : (b == kBufS ? p.ld[kBufS] : p.ld[kBufYp]));
 }
 
-// A chunk layout: element (k, r) of a 64 x 16 chunk lives at k*64 + (r ^ ((k & 3) << 3)).
-// The XOR spreads the four k rows a fragment load touches over both bank halves.
-__host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 3)); }
+// A chunk layout: element (k, r) of a 64 x 16 chunk lives at k*64 + (r ^ ((k & 3) << 2)).
+// A 64-bit fragment load is served per half-warp (lanes r = R..R+3, k = kk..kk+3); the
+// XOR on bits 2-3 of r moves the four k rows to four disjoint 8-bank groups, so each
+// half-warp is one wavefront (rows are 512 B apart and would otherwise collide).
+__host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 2)); }
 
 // ---------------------------------------------------------------- A pre-tiling
 __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
@@ -161,7 +163,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kConsumerWarps * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -206,8 +208,12 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   // the last column block: their DMMAs are skipped, so a ragged tile (srank 46 in a
   // 64-row tile) hands its tensor-pipe cycles to the other CTA on the SM.
   const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
-  const int live_i = min(4, max(0, (static_cast<int>(task.m) - wm * 32 + 7) / 8));
-  const int live_j = min(4, max(0, (static_cast<int>(ncols) - wn * 32 + 7) / 8));
+  // Fragment i of warp (wm, wn) covers rows 8*(2i+wm) .. +7 and fragment j columns
+  // 8*(2j+wn) .. +7: interleaving spreads a ragged tile's live fragments evenly over the
+  // four warps, i.e. over the four SM sub-partitions and their DMMA pipes.
+  const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
+  const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
+  const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
   // Fragment addresses (shared window, bytes) relative to the stage base. A: swizzled
   // 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile.
   std::uint32_t a_off[4][4], b_off[4][4];  // [k step][fragment]
@@ -215,10 +221,10 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   for (int ks = 0; ks < 4; ++ks) {
     const int k = ks * 4 + fk;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a_off[ks][i] = 8u * a_swz(k, wm * 32 + i * 8 + fr);
+    for (int i = 0; i < 4; ++i) a_off[ks][i] = 8u * a_swz(k, (2 * i + wm) * 8 + fr);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int n = wn * 32 + j * 8 + fr;
+      const int n = (2 * j + wn) * 8 + fr;
       b_off[ks][j] = kChunkBytes + (k * kBPitch + n) * 8;
     }
   }
@@ -248,8 +254,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
         for (int j = 0; j < 4; ++j)
           if (i < live_i && j < live_j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    mbar_arrive(&empty[stage]);  // every consumer thread releases the stage after its last read
   }
 
   // epilogue: every valid element of the tile is stored exactly once (zeros for empty tasks)
@@ -257,12 +262,12 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   const std::uint64_t ldc = pick_ld(p, task.cbuf);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int row = wm * 32 + i * 8 + fr;
+    const int row = (2 * i + wm) * 8 + fr;
     if (row >= task.m) continue;
     double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int col = wn * 32 + j * 8 + 2 * fk;
+      const int col = (2 * j + wn) * 8 + 2 * fk;
       if (col + 1 < static_cast<int>(ncols))
         *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
       else if (col < static_cast<int>(ncols))

@@ -1,0 +1,21 @@
+"""The reference's own executor assertions (proj/tests/test_executor.cpp:30-164) re-run on
+the B200 through the C++ drop-in shim hmx_gpu::evaluate (include/hmx_gpu.hpp), on
+instances built by the reference pipeline. The binary is compiled in the build container
+(it needs the reference headers) by `make -C oracle gputest`."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "test_executor_gpu")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="oracle/_ref/test_executor_gpu not built")
+def test_reference_executor_suite_through_shim():
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "checks passed" in out.stdout
