@@ -111,6 +111,8 @@ struct DevState {
   double* w_stage[2] = {nullptr, nullptr};
   double* y_stage[2] = {nullptr, nullptr};
   std::uint64_t resident_bytes = 0;
+  std::uint32_t* tile_counters = nullptr;  // one per GEMM launch, zeroed per evaluation
+  unsigned gemm_grid = 0;                   // resident CTAs of the persistent GEMM
 
   void release_workspace() {
     cudaFree(wp);
@@ -135,6 +137,8 @@ struct DevState {
     release_workspace();
     release_stage();
     cudaFree(tiles);
+    cudaFree(tile_counters);
+    tile_counters = nullptr;
     cudaFree(tasks);
     cudaFree(segs);
     cudaFree(ipmap);
@@ -235,11 +239,15 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   p.segs = d.segs;
   p.q = qq;
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
-  for (const Phase& ph : plan.phases) {
+  HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, plan.phases.size() * sizeof(std::uint32_t), st));
+  for (std::size_t ph_i = 0; ph_i < plan.phases.size(); ++ph_i) {
+    const Phase& ph = plan.phases[ph_i];
     p.tasks = d.tasks + ph.task_begin;
-    const std::uint64_t ctas = std::uint64_t(ph.task_end - ph.task_begin) * col_blocks;
-    if (ctas > 0x7fffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: grid too large");
-    grouped_gemm<<<static_cast<unsigned>(ctas), kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p);
+    const std::uint32_t ntasks = ph.task_end - ph.task_begin;
+    const std::uint64_t tiles = std::uint64_t(ntasks) * col_blocks;
+    if (tiles > 0xfffff000ull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many output tiles");
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, d.gemm_grid));
+    grouped_gemm<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, ntasks, d.tile_counters + ph_i);
     ++*launches;
     HMXG_TRY(mark());
   }
@@ -372,6 +380,13 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
     d.phase_ev.resize(plan.phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    {
+      int per_sm = 0, sms = 0;
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
+      HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
+      d.gemm_grid = static_cast<unsigned>(std::max(1, per_sm) * sms);
+      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size()) * sizeof(std::uint32_t)));
+    }
     // raw generators -> pre-tiled A operands on the device, then the raw copies go away
     double *gd = nullptr, *gb = nullptr, *gv = nullptr;
     TileSrc* srcs = nullptr;

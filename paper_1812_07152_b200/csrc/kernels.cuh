@@ -41,7 +41,7 @@ constexpr int kChunkBytes = kChunkElems * 8;         // 8 KB
 constexpr int kBPitch = kBN + 4;
 constexpr int kBTileBytes = kBPitch * kBK * 8;       // 8704 B
 constexpr int kStageBytes = kChunkBytes + kBTileBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + 1024;  // + barriers + align slack
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + 4 * 8 + 16 + 1024;  // + barriers, tile ring, align slack
 
 struct GemmParams {
   const double* tiles;          // pre-tiled A chunks
@@ -143,21 +143,92 @@ __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__
   }
 }
 
+// One tile's K loop for a consumer warp: LI x LJ live 8 x 8 fragments (compile time).
+// Fragments of k step ks+1 are loaded while step ks multiplies (register double buffer).
+template <int LI, int LJ>
+__device__ __forceinline__ void consume_chunks(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
+                                               std::uint32_t smem_base, const std::uint32_t (&a_off)[4][4],
+                                               const std::uint32_t (&b_off)[4][4], std::uint32_t nchunks,
+                                               std::uint32_t& it) {
+  for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
+    const int stage = it % kStages;
+    mbar_wait(&full[stage], (it / kStages) & 1);
+    const std::uint32_t st = smem_base + stage * kStageBytes;
+    if (LI > 0 && LJ > 0) {
+      double af[2][4], bf[2][4];
+#pragma unroll
+      for (int i = 0; i < LI; ++i) af[0][i] = lds64(st + a_off[0][i]);
+#pragma unroll
+      for (int j = 0; j < LJ; ++j) bf[0][j] = lds64(st + b_off[0][j]);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int cur = ks & 1;
+        if (ks + 1 < 4) {
+#pragma unroll
+          for (int i = 0; i < LI; ++i) af[cur ^ 1][i] = lds64(st + a_off[ks + 1][i]);
+#pragma unroll
+          for (int j = 0; j < LJ; ++j) bf[cur ^ 1][j] = lds64(st + b_off[ks + 1][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < LI; ++i)
+#pragma unroll
+          for (int j = 0; j < LJ; ++j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
+      }
+    }
+    mbar_arrive(&empty[stage]);  // every consumer thread releases the stage after its last read
+  }
+}
+
+// Partial column block (Q not a multiple of 64): runtime-predicated fragments.
+__device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
+                                                 std::uint32_t smem_base, const std::uint32_t (&a_off)[4][4],
+                                                 const std::uint32_t (&b_off)[4][4], std::uint32_t nchunks,
+                                                 std::uint32_t& it, int live_i, int live_j) {
+  for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
+    const int stage = it % kStages;
+    mbar_wait(&full[stage], (it / kStages) & 1);
+    const std::uint32_t st = smem_base + stage * kStageBytes;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = i < live_i ? lds64(st + a_off[ks][i]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = j < live_j ? lds64(st + b_off[ks][j]) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (i < live_i && j < live_j) dmma884(acc[i][j], af[i], bf[j]);
+    }
+    mbar_arrive(&empty[stage]);
+  }
+}
+
 // ---------------------------------------------------------------- grouped GEMM
+// Persistent: gridDim.x = resident CTAs (SMs x occupancy). The producer lane claims output
+// tiles from a per-launch atomic counter in raster order (column block fastest, so a row
+// tile's A chunks are fetched from HBM once and re-served from L2 to every column block),
+// posts each tile id to a 2-slot ring for the consumers, and keeps streaming chunks across
+// tile boundaries: the next tile's first chunks land while the consumers run the
+// current tile's epilogue. Barrier setup happens once per CTA, not once per tile.
+constexpr int kTileRing = 2;
+
 __global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
 grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
-             const __grid_constant__ CUtensorMap tm_s, const GemmParams p) {
+             const __grid_constant__ CUtensorMap tm_s, const GemmParams p, std::uint32_t ntasks,
+             std::uint32_t* __restrict__ tile_counter) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                          ~std::uintptr_t(1023));
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * kStageBytes);
   std::uint64_t* empty = full + kStages;
+  std::uint64_t* tfull = empty + kStages;
+  std::uint64_t* tempty = tfull + kTileRing;
+  std::uint32_t* tring = reinterpret_cast<std::uint32_t*>(tempty + kTileRing);
 
-  // column-block-fastest raster: the CTAs of one row tile run back to back, so its A
-  // chunks are fetched from HBM once and re-served from L2 to every column block
   const std::uint32_t col_blocks = (p.q + kBN - 1) / kBN;
-  const Task task = p.tasks[blockIdx.x / col_blocks];
-  const std::uint32_t c0 = (blockIdx.x % col_blocks) * kBN;
+  const std::uint32_t ntiles = ntasks * col_blocks;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -165,57 +236,54 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps * 32);
     }
+    for (int s = 0; s < kTileRing; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kConsumerWarps * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer: one elected lane streams the chunk sequence
+    // ---------------- producer: one lane claims tiles and streams their chunk sequences
     if (lane == 0) {
-      std::uint32_t it = 0;
-      for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
-        const SegDev sg = p.segs[si];
-        const CUtensorMap* map = sg.bbuf == kBufWp ? &tm_wp : (sg.bbuf == kBufT ? &tm_t : &tm_s);
-        for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
-          const int stage = it % kStages;
-          if (it >= kStages) mbar_wait(&empty[stage], ((it / kStages) - 1) & 1);
-          unsigned char* st = smem + stage * kStageBytes;
-          mbar_expect_tx(&full[stage], kStageBytes);
-          bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
-                   &full[stage]);
-          // coordinates: {column (inner, Q-contiguous), row}
-          tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
+      std::uint32_t it = 0;  // chunk counter across tiles (stage ring position)
+      for (std::uint32_t seq = 0;; ++seq) {
+        const std::uint32_t t = atomicAdd(tile_counter, 1u);
+        const int slot = seq % kTileRing;
+        if (seq >= kTileRing) mbar_wait(&tempty[slot], ((seq / kTileRing) - 1) & 1);
+        tring[slot] = t;
+        mbar_arrive(&tfull[slot]);  // release: the consumers read tring[slot] after the wait
+        if (t >= ntiles) break;
+        const Task task = p.tasks[t / col_blocks];
+        const std::uint32_t c0 = (t % col_blocks) * kBN;
+        for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
+          const SegDev sg = p.segs[si];
+          const CUtensorMap* map = sg.bbuf == kBufWp ? &tm_wp : (sg.bbuf == kBufT ? &tm_t : &tm_s);
+          for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
+            const int stage = it % kStages;
+            if (it >= kStages) mbar_wait(&empty[stage], ((it / kStages) - 1) & 1);
+            unsigned char* st = smem + stage * kStageBytes;
+            mbar_expect_tx(&full[stage], kStageBytes);
+            bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
                      &full[stage]);
+            // coordinates: {column (inner, Q-contiguous), row}
+            tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
+                       &full[stage]);
+          }
         }
       }
     }
     return;
   }
 
-  // ---------------- consumers: 2 x 2 warps of 32 x 32
+  // ---------------- consumers: 2 x 2 warps, interleaved 8 x 8 fragments
   const int wm = warp & 1, wn = warp >> 1;
-  std::uint32_t nchunks = 0;
-  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
-
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
   const int fr = lane >> 2, fk = lane & 3;
-  // Warp-uniform trim of 8-row / 8-column fragments outside the task's valid rows and
-  // the last column block: their DMMAs are skipped, so a ragged tile (srank 46 in a
-  // 64-row tile) hands its tensor-pipe cycles to the other CTA on the SM.
-  const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
-  // Fragment i of warp (wm, wn) covers rows 8*(2i+wm) .. +7 and fragment j columns
-  // 8*(2j+wn) .. +7: interleaving spreads a ragged tile's live fragments evenly over the
-  // four warps, i.e. over the four SM sub-partitions and their DMMA pipes.
-  const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
-  const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
-  const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
   // Fragment addresses (shared window, bytes) relative to the stage base. A: swizzled
-  // 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile.
+  // 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile. Fragment i of warp (wm, wn)
+  // covers rows 8*(2i+wm) .. +7 and fragment j columns 8*(2j+wn) .. +7: interleaving
+  // spreads a ragged tile's live fragments evenly over the four warps.
   std::uint32_t a_off[4][4], b_off[4][4];  // [k step][fragment]
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
@@ -223,55 +291,63 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
 #pragma unroll
     for (int i = 0; i < 4; ++i) a_off[ks][i] = 8u * a_swz(k, (2 * i + wm) * 8 + fr);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = (2 * j + wn) * 8 + fr;
-      b_off[ks][j] = kChunkBytes + (k * kBPitch + n) * 8;
-    }
+    for (int j = 0; j < 4; ++j) b_off[ks][j] = kChunkBytes + (k * kBPitch + (2 * j + wn) * 8 + fr) * 8;
   }
   const std::uint32_t smem_base = smem_u32(smem);
-  for (std::uint32_t it = 0; it < nchunks; ++it) {
-    const int stage = it % kStages;
-    mbar_wait(&full[stage], (it / kStages) & 1);
-    const std::uint32_t st = smem_base + stage * kStageBytes;
-    // register double buffer: fragments of k step ks+1 load while step ks multiplies
-    double af[2][4], bf[2][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[0][i] = lds64(st + a_off[0][i]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bf[0][j] = lds64(st + b_off[0][j]);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int cur = ks & 1;
-      if (ks + 1 < 4) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) af[cur ^ 1][i] = lds64(st + a_off[ks + 1][i]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[cur ^ 1][j] = lds64(st + b_off[ks + 1][j]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (i < live_i && j < live_j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
-    }
-    mbar_arrive(&empty[stage]);  // every consumer thread releases the stage after its last read
-  }
+  std::uint32_t it = 0;
+  for (std::uint32_t seq = 0;; ++seq) {
+    const int slot = seq % kTileRing;
+    mbar_wait(&tfull[slot], (seq / kTileRing) & 1);
+    const std::uint32_t t = tring[slot];
+    mbar_arrive(&tempty[slot]);
+    if (t >= ntiles) break;
+    const Task task = p.tasks[t / col_blocks];
+    const std::uint32_t c0 = (t % col_blocks) * kBN;
+    std::uint32_t nchunks = 0;
+    for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
+    // Warp-uniform trim of fragments outside the task's valid rows / the last column
+    // block: their DMMAs are skipped.
+    const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
+    const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
+    const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
+    const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
 
-  // epilogue: every valid element of the tile is stored exactly once (zeros for empty tasks)
-  double* C = pick_buf(p, task.cbuf);
-  const std::uint64_t ldc = pick_ld(p, task.cbuf);
+    double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = (2 * i + wm) * 8 + fr;
-    if (row >= task.m) continue;
-    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = (2 * j + wn) * 8 + 2 * fk;
-      if (col + 1 < static_cast<int>(ncols))
-        *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-      else if (col < static_cast<int>(ncols))
-        crow[col] = acc[i][j][0];
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
+    // uniformly, once per tile) to a K loop instantiated for their live fragment count.
+    if (live_j == 4) {
+      switch (live_i) {
+        case 4: consume_chunks<4, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
+        case 3: consume_chunks<3, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
+        case 2: consume_chunks<2, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
+        case 1: consume_chunks<1, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
+        default: consume_chunks<0, 0>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
+      }
+    } else {
+      consume_chunks_pred(acc, full, empty, smem_base, a_off, b_off, nchunks, it, live_i, live_j);
+    }
+
+    // epilogue: every valid element of the tile is stored exactly once (zeros for empty tasks)
+    double* C = pick_buf(p, task.cbuf);
+    const std::uint64_t ldc = pick_ld(p, task.cbuf);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (2 * i + wm) * 8 + fr;
+      if (row >= task.m) continue;
+      double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = (2 * j + wn) * 8 + 2 * fk;
+        if (col + 1 < static_cast<int>(ncols))
+          *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        else if (col < static_cast<int>(ncols))
+          crow[col] = acc[i][j][0];
+      }
     }
   }
 }
