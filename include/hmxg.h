@@ -33,7 +33,11 @@ extern "C" {
 /* hmxg_evaluate flags */
 #define HMXG_F_DEVICE_PTRS 0x1u /* W and Y are device pointers on the matrix's (single) device */
 #define HMXG_F_NO_SYNC 0x2u     /* with DEVICE_PTRS: enqueue on `stream` and return */
-#define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0);
+#define HMXG_F_NO_GRAPH 0x8u    /* with DEVICE_PTRS: issue the launches instead of replaying the
+                                   cached CUDA graph of the launch sequence (the graph is keyed
+                                   on W, Y, q, leading dimensions and a non-NULL stream) */
+#define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0; graph
+                                   replays always record them);
                                    read back with hmxg_phase_get */
 
 /*

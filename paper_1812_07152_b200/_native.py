@@ -21,6 +21,7 @@ HMXG_NO_NODE = 0xFFFFFFFF
 HMXG_F_DEVICE_PTRS = 0x1
 HMXG_F_NO_SYNC = 0x2
 HMXG_F_TIME_PHASES = 0x4
+HMXG_F_NO_GRAPH = 0x8
 PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter"}
 
 _u32p = C.POINTER(C.c_uint32)

@@ -112,9 +112,29 @@ struct DevState {
   double* y_stage[2] = {nullptr, nullptr};
   std::uint64_t resident_bytes = 0;
   std::uint32_t* tile_counters = nullptr;  // one per GEMM launch, zeroed per evaluation
+  // CUDA graph of the whole launch sequence for one (W, Y, q, ld, stream, workspace) key:
+  // repeated device-pointer evaluations replay it instead of issuing ~2H+4 launches.
+  struct GraphKey {
+    const double* w = nullptr;
+    double* y = nullptr;
+    std::size_t q = 0, ldw = 0, ldy = 0;
+    cudaStream_t st = nullptr;
+    const double* wp = nullptr;
+    bool operator==(const GraphKey& o) const {
+      return w == o.w && y == o.y && q == o.q && ldw == o.ldw && ldy == o.ldy && st == o.st && wp == o.wp;
+    }
+  } gkey;
+  cudaGraphExec_t gexec = nullptr;
+  std::uint32_t glaunches = 0;
   unsigned gemm_grid = 0;                   // resident CTAs of the persistent GEMM
 
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+    gkey = GraphKey{};
+  }
   void release_workspace() {
+    drop_graph();
     cudaFree(wp);
     cudaFree(yp);
     cudaFree(t);
@@ -209,9 +229,15 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   const std::uint32_t n = static_cast<std::uint32_t>(plan.n);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
   const dim3 eblk(256);
+  // Per-launch timing events. Under graph capture they become external event-record
+  // nodes, so a replayed graph still times every launch.
   std::size_t ev = 0;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HMXG_CUDA(cudaStreamIsCapturing(st, &cap));
+  const bool capturing = cap == cudaStreamCaptureStatusActive;
   auto mark = [&]() -> int {
-    if (time_phases) HMXG_CUDA(cudaEventRecord(d.phase_ev[ev++], st));
+    if (time_phases || capturing)
+      HMXG_CUDA(cudaEventRecordWithFlags(d.phase_ev[ev++], st, capturing ? cudaEventRecordExternal : 0u));
     return HMXG_OK;
   };
   CUtensorMap tm_wp, tm_t, tm_s;
@@ -255,7 +281,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   ++*launches;
   HMXG_TRY(mark());
   HMXG_CUDA(cudaGetLastError());
-  if (time_phases) d.phase_valid = true;
+  if (time_phases || capturing) d.phase_valid = true;
   return HMXG_OK;
 }
 
@@ -502,7 +528,31 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     HMXG_TRY(ensure_workspace(plan, d, q));
     const bool sync = !(flags & HMXG_F_NO_SYNC);
     if (sync) HMXG_CUDA(cudaEventRecord(d.ev0, st));
-    HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, &launches));
+    if (st == nullptr || (flags & HMXG_F_NO_GRAPH)) {
+      HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, &launches));
+    } else {
+      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp};
+      if (!(d.gexec && d.gkey == key)) {
+        d.drop_graph();
+        cudaGraph_t graph = nullptr;
+        HMXG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        std::uint32_t captured = 0;
+        const int rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, false, &captured);
+        const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+        if (rc != HMXG_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          return rc;
+        }
+        if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
+        const cudaError_t ei = cudaGraphInstantiate(&d.gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) return cuda_fail(ei, "cudaGraphInstantiate");
+        d.gkey = key;
+        d.glaunches = captured;
+      }
+      HMXG_CUDA(cudaGraphLaunch(d.gexec, st));
+      launches += d.glaunches;
+    }
     if (sync) {
       HMXG_CUDA(cudaEventRecord(d.ev1, st));
       HMXG_CUDA(cudaEventSynchronize(d.ev1));

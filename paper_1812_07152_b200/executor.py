@@ -200,11 +200,12 @@ class Evaluator:
 
     def evaluate_device(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
                         stream: int = 0, sync: bool = False, stats: EvalStats | None = None,
-                        time_phases: bool = False) -> None:
+                        time_phases: bool = False, graph: bool = True) -> None:
         """Device-pointer evaluation (single-device context): W/Y already in HBM,
         enqueued on ``stream`` (a cudaStream_t as int, 0 = internal stream)."""
         n = self.cds.n
-        flags = N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC) | (N.HMXG_F_TIME_PHASES if time_phases else 0)
+        flags = (N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC) | (N.HMXG_F_TIME_PHASES if time_phases else 0)
+                 | (0 if graph else N.HMXG_F_NO_GRAPH))
         st = N.Stats()
         _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
                                       flags, C.c_void_p(stream) if stream else None, C.byref(st)))

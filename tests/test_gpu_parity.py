@@ -134,3 +134,25 @@ def test_device_pointer_path():
     torch.cuda.synchronize()
     y = yd.cpu().numpy().T
     assert np.array_equal(y, ev.evaluate(w))
+
+
+def test_graph_replay_matches_direct_launches():
+    import torch
+
+    spec, _ = config("cfg2-h2b")
+    inst = build_instance(spec)
+    n, q = inst.cds.n, 96
+    ev = Evaluator(inst.cds)
+    s = torch.cuda.Stream()
+    w = torch.randn((q, n), dtype=torch.float64, device="cuda")
+    y_direct, y_graph = torch.empty_like(w), torch.empty_like(w)
+    ev.evaluate_device(w.data_ptr(), y_direct.data_ptr(), q, stream=s.cuda_stream, sync=True, graph=False)
+    for _ in range(2):  # capture, then replay
+        ev.evaluate_device(w.data_ptr(), y_graph.data_ptr(), q, stream=s.cuda_stream, sync=True)
+    assert torch.equal(y_direct, y_graph)
+    w.copy_(torch.randn_like(w))  # same pointers, new data: the replay must read it
+    ev.evaluate_device(w.data_ptr(), y_graph.data_ptr(), q, stream=s.cuda_stream, sync=True)
+    ev.evaluate_device(w.data_ptr(), y_direct.data_ptr(), q, stream=s.cuda_stream, sync=True, graph=False)
+    assert torch.equal(y_direct, y_graph)
+    y = y_graph.cpu().numpy().T
+    assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w.cpu().numpy().T)) <= TOL
