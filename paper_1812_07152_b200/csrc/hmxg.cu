@@ -410,7 +410,10 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
       int per_sm = 0, sms = 0;
       HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
       HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
-      d.gemm_grid = static_cast<unsigned>(std::max(1, per_sm) * sms);
+#ifndef HMXG_GEMM_CTAS_PER_SM
+#define HMXG_GEMM_CTAS_PER_SM 3
+#endif
+      d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
       HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size()) * sizeof(std::uint32_t)));
     }
     // raw generators -> pre-tiled A operands on the device, then the raw copies go away

@@ -156,3 +156,26 @@ def test_graph_replay_matches_direct_launches():
     assert torch.equal(y_direct, y_graph)
     y = y_graph.cpu().numpy().T
     assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w.cpu().numpy().T)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cfg3-h2b", "cfg4-h2b", "cfg5-hss", "cfg5-h2b"])
+def test_configs_full_size_column_subset(name):
+    """BASELINE configs at full size: the full-Q evaluation's columns are checked on a seeded
+    subset against the oracle (Y[:,c] depends only on W[:,c]), and evaluating
+    the subset alone must reproduce those columns bit for bit."""
+    spec, q = config(name)
+    inst = build_instance(spec)
+    n = inst.cds.n
+    ev = Evaluator(inst.cds)
+    rng = np.random.default_rng(11)
+    w = np.asfortranarray(rng.standard_normal((n, q)))
+    y = ev.evaluate(w)
+    cols = np.sort(rng.choice(q, size=6, replace=False))
+    wsub = np.asfortranarray(w[:, cols])
+    assert oracle.rel_frob(y[:, cols], oracle.oracle_evaluate(inst.cds, wsub)) <= TOL
+    assert np.array_equal(ev.evaluate(wsub), y[:, cols])
+    # linearity at full size on two columns
+    y2 = ev.evaluate(np.asfortranarray(np.stack([w[:, cols[0]] * 3.0 + w[:, cols[1]], w[:, cols[1]]], axis=1)))
+    assert oracle.rel_frob(y2[:, 0], 3.0 * y[:, cols[0]] + y[:, cols[1]]) <= TOL
+    ev.close()
+    inst.close()
