@@ -300,7 +300,7 @@ def ours(args) -> None:
     flops_step = cds.flops(q_total)
     value = flops_step / (ms_per_step * 1e-3) / 1e9
 
-    # dominant kernel: the launch with the largest share of the step
+    # dominant kernel: the launch with the largest share of the step (the DAG launch)
     shares = [m / local_ms for m in phase_ms]
     dom = max(range(len(phase_ms)), key=lambda i: phase_ms[i])
     pinfo = phase_info[dom]
@@ -308,14 +308,21 @@ def ours(args) -> None:
     dom_flops = pinfo["flops_per_col"] * q
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json"), {}) or {}
     traffic = (prof.get(args.config) or {}).get("dominant_dram_bytes_per_launch")
+    kname = {"dag": "eval_dag (every GEMM tile of every tree level)"}.get(pinfo["kind"], f"{pinfo['kind']} L{pinfo['level']}")
     roofline = {"bound": "tensor", "achieved": dom_flops / (dom_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": dom_flops / (dom_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                "traffic": traffic, "kernel": f"grouped_gemm<false> {pinfo['kind']} (level {pinfo['level']})",
-                "share_of_step": shares[dom],
+                "traffic": traffic, "kernel": kname, "share_of_step": shares[dom],
                 "peak_source": "measured FP64 DMMA peak on this pool (profiles/r01_fp64_peak.txt); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "algorithmic_flops_per_launch": dom_flops,
                 "algorithmic_bytes_per_launch": pinfo["gen_bytes"] + pinfo["io_bytes_per_col"] * q}
+    # diagnostic (untimed): the same evaluation as level-by-level launches, per-launch times
+    with torch.cuda.stream(stream):
+        ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=stream.cuda_stream, time_phases=True, graph=False,
+                           levels=True)
+    torch.cuda.synchronize()
+    level_phases = [{"kind": p["kind"], "level": p["level"], "ms": round(p["ms"], 4),
+                     "tflops": round(p["flops_per_col"] * q / max(p["ms"], 1e-9) / 1e9, 2)} for p in ev.phases()]
     # whole-evaluation roofline: max(flops / P_fp64, bytes / HBM)
     t_roof = max(flops_step / world / (FP64_PEAK_TFLOPS * 1e12), cds.bytes(q) / (hbm_peak() * 1e9))
     eval_roofline = {"time_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms_per_step,
@@ -382,6 +389,7 @@ def ours(args) -> None:
             "clocks": {"sm_mhz": clk_all[0]["sm_mhz"], "sm_max_mhz": clk_all[0]["sm_max_mhz"],
                        "reasons": sorted({r for c in clk_all for r in c["reasons"]})},
             "phases_ms": phases_out,
+            "level_launch_breakdown": level_phases,
         }
         print(json.dumps(line), flush=True)
     ev.close()

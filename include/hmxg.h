@@ -36,6 +36,9 @@ extern "C" {
 #define HMXG_F_NO_GRAPH 0x8u    /* with DEVICE_PTRS: issue the launches instead of replaying the
                                    cached CUDA graph of the launch sequence (the graph is keyed
                                    on W, Y, q, leading dimensions and a non-NULL stream) */
+#define HMXG_F_LEVEL_LAUNCHES 0x10u /* run the level-by-level launch sequence (one launch per
+                                       tree level) instead of the single whole-evaluation DAG
+                                       launch: same results, per-launch timing breakdown */
 #define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0; graph
                                    replays always record them);
                                    read back with hmxg_phase_get */
@@ -95,14 +98,16 @@ typedef struct hmxg_info {
   uint64_t d_elems, b_elems, v_elems; /* |Dgen|, |Bgen|, |Vgen| */
   uint64_t skel_rows;                 /* sum of active sranks (T/S rows) */
   uint32_t num_devices;
-  uint32_t launches_per_eval;         /* kernels per evaluate call per device */
+  uint32_t launches_per_eval;         /* kernels per evaluate call per device (3: permute-in,
+                                         the whole-evaluation DAG launch, permute-out) */
   double flops_per_col;               /* 2*(2|V|+|B|+|D|) */
   uint64_t device_bytes;              /* resident generator + table bytes per device */
 } hmxg_info;
 
 /* One launch of the per-evaluation launch sequence (SURVEY §7.3 / DESIGN.md):
  * kind 0 gather, 1 upward (level = subtree height), 2 far+downward (level = depth),
- * 3 near+leaf-downward, 4 scatter. Byte/flop fields are ALGORITHMIC (each operand block
+ * 3 near+leaf-downward, 4 scatter, 5 the whole-evaluation DAG launch (every GEMM tile of
+ * every level; the default sequence is gather, DAG, scatter). Byte/flop fields are ALGORITHMIC (each operand block
  * counted once): the roofline numerators of bench.py. last_ms is the device time of that
  * launch in the last evaluation run with HMXG_F_TIME_PHASES on device 0. */
 typedef struct hmxg_phase {

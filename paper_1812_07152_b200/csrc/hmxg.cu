@@ -112,6 +112,17 @@ struct DevState {
   double* y_stage[2] = {nullptr, nullptr};
   std::uint64_t resident_bytes = 0;
   std::uint32_t* tile_counters = nullptr;  // one per GEMM launch, zeroed per evaluation
+  // whole-evaluation DAG launch: work items (built per column count) and counters
+  struct DagItems {
+    std::size_t q = 0;
+    std::uint64_t* items = nullptr;
+    std::uint32_t nitems = 0;
+  };
+  DagItems dag[3];                    // item lists of the last few column counts
+  std::uint32_t dag_next = 0;
+  std::uint32_t* dag_done = nullptr;  // claim counter + done counters (sized for the largest q)
+  std::size_t dag_done_cap = 0;
+  std::uint32_t* node_tiles = nullptr;
   // CUDA graph of the whole launch sequence for one (W, Y, q, ld, stream, workspace) key:
   // repeated device-pointer evaluations replay it instead of issuing ~2H+4 launches.
   struct GraphKey {
@@ -120,11 +131,14 @@ struct DevState {
     std::size_t q = 0, ldw = 0, ldy = 0;
     cudaStream_t st = nullptr;
     const double* wp = nullptr;
+    bool levels = false;
     bool operator==(const GraphKey& o) const {
-      return w == o.w && y == o.y && q == o.q && ldw == o.ldw && ldy == o.ldy && st == o.st && wp == o.wp;
+      return w == o.w && y == o.y && q == o.q && ldw == o.ldw && ldy == o.ldy && st == o.st && wp == o.wp &&
+             levels == o.levels;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
+  bool last_levels = false;  // launch sequence of the last evaluation (phase reporting)
   std::uint32_t glaunches = 0;
   unsigned gemm_grid = 0;                   // resident CTAs of the persistent GEMM
 
@@ -159,6 +173,15 @@ struct DevState {
     cudaFree(tiles);
     cudaFree(tile_counters);
     tile_counters = nullptr;
+    for (auto& e : dag) {
+      cudaFree(e.items);
+      e = DagItems{};
+    }
+    cudaFree(dag_done);
+    cudaFree(node_tiles);
+    dag_done = nullptr;
+    dag_done_cap = 0;
+    node_tiles = nullptr;
     cudaFree(tasks);
     cudaFree(segs);
     cudaFree(ipmap);
@@ -222,9 +245,56 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
   return HMXG_OK;
 }
 
-// Enqueue one full evaluation of q columns: W (ldw) -> Y (ldy), device pointers.
+// Work items of the whole-evaluation DAG launch for q columns, in topological order:
+// levels in launch order (upward by height, far+downward by depth, leaves), each level's
+// row tiles in task order with the column block fastest (so a row tile's A chunks are
+// re-served from L2 to all column blocks).
+std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q) {
+  const std::uint32_t ncb = (q + kBN - 1) / kBN;
+  std::vector<std::uint64_t> items;
+  for (const Phase& ph : plan.phases)
+    for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+      for (std::uint32_t cb = 0; cb < ncb; ++cb) items.push_back(make_item(kItemGemm, cb, t));
+  return items;
+}
+
+std::size_t dag_done_words(const Plan& plan, std::size_t q) {
+  const std::size_t ncb = (q + kBN - 1) / kBN;
+  return 1 + 2 * std::size_t(plan.num_nodes) * ncb;
+}
+
+// Item list and counters for q columns (built on first use, cached for a few q).
+int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, const DevState::DagItems** out) {
+  for (const auto& e : d.dag)
+    if (e.items && e.q == q) {
+      *out = &e;
+      return HMXG_OK;
+    }
+  DevState::DagItems& e = d.dag[d.dag_next++ % 3];
+  HMXG_CUDA(cudaStreamSynchronize(st));  // the slot's previous list may still be in use
+  cudaFree(e.items);
+  e = DevState::DagItems{};
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q));
+  if (items.size() >= 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many work items");
+  HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
+  const std::size_t words = dag_done_words(plan, q);
+  if (words > d.dag_done_cap) {
+    cudaFree(d.dag_done);
+    d.dag_done = nullptr;
+    HMXG_CUDA(cudaMalloc(&d.dag_done, words * sizeof(std::uint32_t)));
+    d.dag_done_cap = words;
+  }
+  HMXG_CUDA(cudaStreamSynchronize(st));
+  e.nitems = static_cast<std::uint32_t>(items.size());
+  e.q = q;
+  *out = &e;
+  return HMXG_OK;
+}
+
+// Default: one whole-evaluation DAG launch. `levels`: the level-by-level launch sequence
+// (permute-in, one launch per tree level, permute-out) for per-launch breakdowns.
 int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw, double* y,
-                 std::size_t ldy, std::size_t q, cudaStream_t st, bool time_phases,
+                 std::size_t ldy, std::size_t q, cudaStream_t st, bool time_phases, bool levels,
                  std::uint32_t* launches) {
   const std::uint32_t n = static_cast<std::uint32_t>(plan.n);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
@@ -245,13 +315,6 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   HMXG_TRY(make_map(&tm_wp, d.wp, plan.rows_pad, q, ldq));
   HMXG_TRY(make_map(&tm_t, d.t, plan.skel_rows, q, ldq));
   HMXG_TRY(make_map(&tm_s, d.s, plan.skel_rows, q, ldq));
-  HMXG_TRY(mark());
-  const dim3 pgrid((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
-  if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
-  permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
-  ++*launches;
-  HMXG_TRY(mark());
-
   GemmParams p{};
   p.tiles = d.tiles;
   p.buf[kBufWp] = d.wp;
@@ -264,6 +327,44 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   p.ld[kBufYp] = ldq;
   p.segs = d.segs;
   p.q = qq;
+  if (!levels) {
+    const DevState::DagItems* di = nullptr;
+    for (const auto& e : d.dag)
+      if (e.items && e.q == q) di = &e;
+    if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
+    DagParams dp{};
+    dp.items = di->items;
+    dp.nitems = di->nitems;
+    dp.claim = d.dag_done;
+    dp.done = d.dag_done + 1;
+    dp.node_tiles = d.node_tiles;
+    dp.ncb = (qq + kBN - 1) / kBN;
+    dp.nodes = plan.num_nodes;
+    p.tasks = d.tasks;
+    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
+    HMXG_TRY(mark());
+    const dim3 pgrid2((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
+    if (pgrid2.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
+    permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
+    ++*launches;
+    HMXG_TRY(mark());
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
+    eval_dag<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+    ++*launches;
+    HMXG_TRY(mark());
+    permute_out<<<pgrid2, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq);
+    ++*launches;
+    HMXG_TRY(mark());
+    HMXG_CUDA(cudaGetLastError());
+    if (time_phases || capturing) d.phase_valid = true;
+    return HMXG_OK;
+  }
+  HMXG_TRY(mark());
+  const dim3 pgrid((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
+  if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
+  permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
+  ++*launches;
+  HMXG_TRY(mark());
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
   HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, plan.phases.size() * sizeof(std::uint32_t), st));
   for (std::size_t ph_i = 0; ph_i < plan.phases.size(); ++ph_i) {
@@ -300,7 +401,7 @@ int copy_cols(double* dst, std::size_t lddst, const double* src, std::size_t lds
 // double-buffered staging, copies on their own streams so PCIe traffic in both
 // directions overlaps the kernels.
 int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size_t ldw, double* Y,
-                       std::size_t ldy, std::size_t c0, std::size_t c1, bool time_phases,
+                       std::size_t ldy, std::size_t c0, std::size_t c1, bool time_phases, bool levels,
                        std::uint32_t* launches) {
   const std::size_t n = plan.n, qg = c1 - c0;
   const std::size_t cq = std::min(qg, kChunkCols);
@@ -318,7 +419,10 @@ int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size
     // output buffer b is free once the copy-out of chunk k-2 finished
     if (k >= 2) HMXG_CUDA(cudaStreamWaitEvent(d.comp, d.ev_out[b], 0));
     if (k == 0) HMXG_CUDA(cudaEventRecord(d.ev0, d.comp));
-    HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, time_phases && k == 0, launches));
+    const DevState::DagItems* di = nullptr;
+    if (!levels) HMXG_TRY(ensure_dag(plan, d, m, d.comp, &di));
+    HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, time_phases && k == 0, levels,
+                          launches));
     HMXG_CUDA(cudaEventRecord(d.ev_done[b], d.comp));
     if (k + 1 == chunks) HMXG_CUDA(cudaEventRecord(d.ev1, d.comp));
     HMXG_CUDA(cudaStreamWaitEvent(d.d2h, d.ev_done[b], 0));
@@ -379,7 +483,7 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
     info->b_elems = plan.b_elems;
     info->v_elems = plan.v_elems;
     info->skel_rows = plan.skel_rows;
-    info->launches_per_eval = static_cast<std::uint32_t>(plan.phases.size() + 2);
+    info->launches_per_eval = 3;
     info->flops_per_col = 2.0 * (2.0 * plan.v_elems + plan.b_elems + plan.d_elems);
   }
   return HMXG_OK;
@@ -406,9 +510,14 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
     d.phase_ev.resize(plan.phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_CUDA(cudaFuncSetAttribute(eval_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     {
       int per_sm = 0, sms = 0;
+      int per_sm_dag = 0;
       HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dag, eval_dag, kThreads, kSmemBytes));
+      // eval_dag relies on every CTA of its grid being resident (items wait on earlier items)
+      per_sm = std::min(per_sm, per_sm_dag);
       HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
 #ifndef HMXG_GEMM_CTAS_PER_SM
 #define HMXG_GEMM_CTAS_PER_SM 3
@@ -441,6 +550,7 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
     HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
     HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
     HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
     d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
                        4 * plan.ipmap.size();
@@ -466,23 +576,35 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   info->v_elems = p.v_elems;
   info->skel_rows = p.skel_rows;
   info->num_devices = static_cast<std::uint32_t>(mat->devs.size());
-  info->launches_per_eval = static_cast<std::uint32_t>(p.phases.size() + 2);
+  info->launches_per_eval = 3;  // permute-in, eval_dag, permute-out
   info->flops_per_col = 2.0 * (2.0 * p.v_elems + p.b_elems + p.d_elems);
   info->device_bytes = mat->devs.empty() ? 0 : mat->devs[0].resident_bytes;
   return HMXG_OK;
 }
 
+// The launch sequence of the most recent evaluation: the DAG sequence (permute-in,
+// eval_dag, permute-out) by default, the level sequence after HMXG_F_LEVEL_LAUNCHES.
 int hmxg_phase_count(const hmxg_mat* mat) {
-  return mat ? static_cast<int>(mat->plan.phases.size() + 2) : -1;
+  if (!mat) return -1;
+  return mat->devs[0].last_levels ? static_cast<int>(mat->plan.phases.size() + 2) : 3;
 }
 
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
   const Plan& p = mat->plan;
-  const std::uint32_t count = static_cast<std::uint32_t>(p.phases.size() + 2);
+  const bool levels = mat->devs[0].last_levels;
+  const std::uint32_t count = static_cast<std::uint32_t>(levels ? p.phases.size() + 2 : 3);
   if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
   std::memset(out, 0, sizeof *out);
-  if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
+  if (!levels && idx == 1) {  // the whole-evaluation DAG launch: every GEMM tile
+    out->kind = 5;
+    for (const Phase& ph : p.phases) {
+      out->tiles += ph.task_end - ph.task_begin;
+      out->flops_per_col += ph.flops_per_col;
+      out->gen_bytes += ph.gen_bytes;
+      out->io_bytes_per_col += ph.io_bytes_per_col;
+    }
+  } else if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
     out->kind = idx == 0 ? 0 : 4;
     out->tiles = static_cast<std::uint32_t>((p.n + 31) / 32);
     out->io_bytes_per_col = 16.0 * p.n;
@@ -519,6 +641,8 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
   std::lock_guard<std::mutex> lock(mat->mu);
   const Plan& plan = mat->plan;
   const bool time_phases = flags & HMXG_F_TIME_PHASES;
+  const bool levels = flags & HMXG_F_LEVEL_LAUNCHES;
+  for (auto& dv : mat->devs) dv.last_levels = levels;
   std::uint32_t launches = 0;
   float dev_ms = 0.f;
 
@@ -529,18 +653,20 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     HMXG_CUDA(cudaSetDevice(d.dev));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.comp;
     HMXG_TRY(ensure_workspace(plan, d, q));
+    const DevState::DagItems* di = nullptr;
+    if (!levels) HMXG_TRY(ensure_dag(plan, d, q, st ? st : d.comp, &di));
     const bool sync = !(flags & HMXG_F_NO_SYNC);
     if (sync) HMXG_CUDA(cudaEventRecord(d.ev0, st));
     if (st == nullptr || (flags & HMXG_F_NO_GRAPH)) {
-      HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, &launches));
+      HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &launches));
     } else {
-      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp};
+      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, levels};
       if (!(d.gexec && d.gkey == key)) {
         d.drop_graph();
         cudaGraph_t graph = nullptr;
         HMXG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         std::uint32_t captured = 0;
-        const int rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, false, &captured);
+        const int rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, false, levels, &captured);
         const cudaError_t ec = cudaStreamEndCapture(st, &graph);
         if (rc != HMXG_OK) {
           if (graph) cudaGraphDestroy(graph);
@@ -570,7 +696,8 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       if (cut[g + 1] == cut[g]) continue;
       DevState& d = mat->devs[g];
       HMXG_CUDA(cudaSetDevice(d.dev));
-      HMXG_TRY(enqueue_host_shard(plan, d, W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0, &launches));
+      HMXG_TRY(enqueue_host_shard(plan, d, W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0, levels,
+                                  &launches));
     }
     for (std::size_t g = 0; g < G; ++g) {
       if (cut[g + 1] == cut[g]) continue;

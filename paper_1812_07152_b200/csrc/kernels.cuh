@@ -41,7 +41,6 @@ constexpr int kChunkBytes = kChunkElems * 8;         // 8 KB
 constexpr int kBPitch = kBN + 4;
 constexpr int kBTileBytes = kBPitch * kBK * 8;       // 8704 B
 constexpr int kStageBytes = kChunkBytes + kBTileBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + 4 * 8 + 16 + 1024;  // + barriers, tile ring, align slack
 
 struct GemmParams {
   const double* tiles;          // pre-tiled A chunks
@@ -205,150 +204,292 @@ __device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std:
   }
 }
 
-// ---------------------------------------------------------------- grouped GEMM
-// Persistent: gridDim.x = resident CTAs (SMs x occupancy). The producer lane claims output
-// tiles from a per-launch atomic counter in raster order (column block fastest, so a row
-// tile's A chunks are fetched from HBM once and re-served from L2 to every column block),
-// posts each tile id to a 2-slot ring for the consumers, and keeps streaming chunks across
-// tile boundaries: the next tile's first chunks land while the consumers run the
-// current tile's epilogue. Barrier setup happens once per CTA, not once per tile.
-constexpr int kTileRing = 2;
+// ---------------------------------------------------------------- tile bodies
+// Shared-memory carve-up of one CTA (both GEMM kernels): kStages x {A chunk, B tile}, the
+// stage barriers, a kTileRing-deep ring of claimed work items and their barriers.
+constexpr int kTileRing = 4;
+constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * 8 + 1024;
 
+struct CtaSmem {
+  unsigned char* stage;    // kStages * kStageBytes, 1024-byte aligned
+  std::uint64_t* full;     // [kStages]
+  std::uint64_t* empty;    // [kStages]
+  std::uint64_t* tfull;    // [kTileRing]
+  std::uint64_t* tempty;   // [kTileRing]
+  std::uint64_t* tring;    // [kTileRing] claimed work items
+};
+
+__device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
+  CtaSmem c;
+  c.stage = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                             ~std::uintptr_t(1023));
+  c.full = reinterpret_cast<std::uint64_t*>(c.stage + kStages * kStageBytes);
+  c.empty = c.full + kStages;
+  c.tfull = c.empty + kStages;
+  c.tempty = c.tfull + kTileRing;
+  c.tring = c.tempty + kTileRing;
+  return c;
+}
+
+__device__ __forceinline__ void init_barriers(const CtaSmem& c) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&c.full[s], 1);
+      mbar_init(&c.empty[s], kConsumerWarps * 32);
+    }
+    for (int s = 0; s < kTileRing; ++s) {
+      mbar_init(&c.tfull[s], 1);
+      mbar_init(&c.tempty[s], kConsumerWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// Producer lane: post a claimed work item to the ring (waits for the slot to be free).
+__device__ __forceinline__ void post_item(const CtaSmem& c, std::uint32_t seq, std::uint64_t item) {
+  const int slot = seq % kTileRing;
+  if (seq >= kTileRing) mbar_wait(&c.tempty[slot], ((seq / kTileRing) - 1) & 1);
+  c.tring[slot] = item;
+  mbar_arrive(&c.tfull[slot]);  // release: consumers read tring[slot] after their wait
+}
+
+// Consumers: fetch the next work item from the ring.
+__device__ __forceinline__ std::uint64_t take_item(const CtaSmem& c, std::uint32_t seq) {
+  const int slot = seq % kTileRing;
+  mbar_wait(&c.tfull[slot], (seq / kTileRing) & 1);
+  const std::uint64_t item = c.tring[slot];
+  mbar_arrive(&c.tempty[slot]);
+  return item;
+}
+
+// Producer lane: stream the A chunks and B tiles of one GEMM tile. `wait_dep(seg)` runs
+// before a segment's first load (the DAG kernel's dependency wait; a no-op per level).
+template <class WaitDep>
+__device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
+                                                  std::uint32_t c0, const CUtensorMap* tm_wp, const CUtensorMap* tm_t,
+                                                  const CUtensorMap* tm_s, std::uint32_t& it, WaitDep&& wait_dep) {
+  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
+    const SegDev sg = p.segs[si];
+    wait_dep(sg);
+    const CUtensorMap* map = sg.bbuf == kBufWp ? tm_wp : (sg.bbuf == kBufT ? tm_t : tm_s);
+    for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
+      const int stage = it % kStages;
+      if (it >= kStages) mbar_wait(&c.empty[stage], ((it / kStages) - 1) & 1);
+      unsigned char* st = c.stage + stage * kStageBytes;
+      mbar_expect_tx(&c.full[stage], kStageBytes);
+      bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
+               &c.full[stage]);
+      // coordinates: {column (inner, Q-contiguous), row}
+      tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
+                 &c.full[stage]);
+    }
+  }
+}
+
+// Per-thread fragment address table of a consumer warp (shared window, bytes, relative to
+// a stage). A: swizzled 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile. Fragment
+// i of warp (wm, wn) covers rows 8*(2i+wm) .. +7 and fragment j columns 8*(2j+wn) .. +7:
+// interleaving spreads a ragged tile's live fragments evenly over the four warps.
+struct FragAddr {
+  std::uint32_t a[4][4], b[4][4];  // [k step][fragment]
+};
+
+__device__ __forceinline__ FragAddr frag_addresses(int wm, int wn, int fr, int fk) {
+  FragAddr f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k = ks * 4 + fk;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f.a[ks][i] = 8u * a_swz(k, (2 * i + wm) * 8 + fr);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) f.b[ks][j] = kChunkBytes + (k * kBPitch + (2 * j + wn) * 8 + fr) * 8;
+  }
+  return f;
+}
+
+// Consumers: the K loop and epilogue of one GEMM tile (each element stored exactly once).
+__device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
+                                                  std::uint32_t c0, const FragAddr& fa, std::uint32_t& it) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
+  std::uint32_t nchunks = 0;
+  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
+  // Warp-uniform trim of fragments outside the task's valid rows / the last column block.
+  const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
+  const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
+  const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
+  const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
+  // uniformly, once per tile) to a K loop instantiated for their live fragment count.
+  const std::uint32_t base = smem_u32(c.stage);
+  if (live_j == 4) {
+    switch (live_i) {
+      case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+      case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+      case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+      case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+      default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+    }
+  } else {
+    consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it, live_i, live_j);
+  }
+
+  double* C = pick_buf(p, task.cbuf);
+  const std::uint64_t ldc = pick_ld(p, task.cbuf);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = (2 * i + wm) * 8 + fr;
+    if (row >= task.m) continue;
+    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = (2 * j + wn) * 8 + 2 * fk;
+      if (col + 1 < static_cast<int>(ncols))
+        *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      else if (col < static_cast<int>(ncols))
+        crow[col] = acc[i][j][0];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- level-launch GEMM
+// Persistent: gridDim.x = resident CTAs (SMs x occupancy). The producer lane claims output
+// tiles of one level from a per-launch atomic counter in raster order (column block
+// fastest, so a row tile's A chunks are fetched from HBM once and re-served from L2 to
+// every column block) and keeps streaming chunks across tile boundaries: the next tile's
+// first chunks land while the consumers run the current tile's epilogue. Used for the
+// per-launch breakdown (HMXG_F_LEVEL_LAUNCHES); evaluations run eval_dag.
 __global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
 grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
              const __grid_constant__ CUtensorMap tm_s, const GemmParams p, std::uint32_t ntasks,
              std::uint32_t* __restrict__ tile_counter) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
-                                                         ~std::uintptr_t(1023));
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kStages * kStageBytes);
-  std::uint64_t* empty = full + kStages;
-  std::uint64_t* tfull = empty + kStages;
-  std::uint64_t* tempty = tfull + kTileRing;
-  std::uint32_t* tring = reinterpret_cast<std::uint32_t*>(tempty + kTileRing);
-
+  const CtaSmem c = carve_smem(smem_raw);
   const std::uint32_t col_blocks = (p.q + kBN - 1) / kBN;
   const std::uint32_t ntiles = ntasks * col_blocks;
+  init_barriers(c);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps * 32);
-    }
-    for (int s = 0; s < kTileRing; ++s) {
-      mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kConsumerWarps * 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
   if (warp == kConsumerWarps) {
-    // ---------------- producer: one lane claims tiles and streams their chunk sequences
     if (lane == 0) {
-      std::uint32_t it = 0;  // chunk counter across tiles (stage ring position)
+      std::uint32_t it = 0;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t t = atomicAdd(tile_counter, 1u);
-        const int slot = seq % kTileRing;
-        if (seq >= kTileRing) mbar_wait(&tempty[slot], ((seq / kTileRing) - 1) & 1);
-        tring[slot] = t;
-        mbar_arrive(&tfull[slot]);  // release: the consumers read tring[slot] after the wait
+        post_item(c, seq, t);
         if (t >= ntiles) break;
-        const Task task = p.tasks[t / col_blocks];
-        const std::uint32_t c0 = (t % col_blocks) * kBN;
-        for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
-          const SegDev sg = p.segs[si];
-          const CUtensorMap* map = sg.bbuf == kBufWp ? &tm_wp : (sg.bbuf == kBufT ? &tm_t : &tm_s);
-          for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
-            const int stage = it % kStages;
-            if (it >= kStages) mbar_wait(&empty[stage], ((it / kStages) - 1) & 1);
-            unsigned char* st = smem + stage * kStageBytes;
-            mbar_expect_tx(&full[stage], kStageBytes);
-            bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
-                     &full[stage]);
-            // coordinates: {column (inner, Q-contiguous), row}
-            tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
-                       &full[stage]);
-          }
-        }
+        produce_gemm_tile(p, c, p.tasks[t / col_blocks], (t % col_blocks) * kBN, &tm_wp, &tm_t, &tm_s, it,
+                          [](const SegDev&) {});
+      }
+    }
+    return;
+  }
+  const FragAddr fa = frag_addresses(warp & 1, warp >> 1, lane >> 2, lane & 3);
+  std::uint32_t it = 0;
+  for (std::uint32_t seq = 0;; ++seq) {
+    const std::uint64_t t = take_item(c, seq);
+    if (t >= ntiles) break;
+    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks) * kBN, fa, it);
+  }
+}
+
+// ---------------------------------------------------------------- whole-evaluation DAG
+// One persistent launch runs every GEMM tile of every tree level (between the permute-in
+// and permute-out kernels). Work items are claimed in a host-built topological order
+// (every dependency of an item precedes it), so the lowest unfinished item can always run
+// and, with all CTAs of the grid resident, the kernel cannot deadlock. Dependencies are
+// per (node, column block): before streaming a segment, a GEMM tile's producer waits until
+// every row tile of the segment's source node has been stored for the same column block
+// (T or S). There are no level boundaries: a level's first tiles start while the
+// previous level's last tiles finish, and there is one launch instead of ~2H.
+enum ItemKind : std::uint32_t { kItemGemm = 0, kItemEnd = 3 };
+__host__ __device__ __forceinline__ std::uint64_t make_item(std::uint32_t kind, std::uint32_t cb, std::uint32_t idx) {
+  return (static_cast<std::uint64_t>(kind) << 56) | (static_cast<std::uint64_t>(cb) << 32) | idx;
+}
+
+struct DagParams {
+  const std::uint64_t* items;
+  std::uint32_t nitems;
+  std::uint32_t* claim;        // work-item counter (zeroed per evaluation)
+  std::uint32_t* done;         // [T: nodes*ncb | S: nodes*ncb] warp signals (zeroed)
+  const std::uint32_t* node_tiles;
+  std::uint32_t ncb, nodes;
+};
+
+__device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const std::uint32_t* p, std::uint32_t target) {
+  if (ld_acquire(p) >= target) return;
+  unsigned ns = 32;
+  while (ld_acquire(p) < target) {
+    __nanosleep(ns);
+    ns = min(ns * 2, 256u);
+  }
+}
+// A consumer warp has stored its part of an item: publish it. __syncwarp orders the
+// lanes' stores before lane 0's release-reduction at gpu scope (no CTA barrier, no L1
+// invalidating fence). Counters therefore count warps: targets are kConsumerWarps x items.
+__device__ __forceinline__ void warp_signal(std::uint32_t* counter) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(counter) : "memory");
+}
+// Lane 0 waits (acquire), then the warp proceeds.
+__device__ __forceinline__ void warp_wait(const std::uint32_t* counter, std::uint32_t target) {
+  if ((threadIdx.x & 31) == 0) spin_until(counter, target);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
+eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
+         const __grid_constant__ CUtensorMap tm_s, const GemmParams p, const DagParams d) {
+  extern __shared__ unsigned char smem_raw[];
+  const CtaSmem c = carve_smem(smem_raw);
+  init_barriers(c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  std::uint32_t* const done_t = d.done;
+  std::uint32_t* const done_s = done_t + static_cast<std::uint64_t>(d.nodes) * d.ncb;
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      std::uint32_t it = 0;
+      for (std::uint32_t seq = 0;; ++seq) {
+        const std::uint32_t q = atomicAdd(d.claim, 1u);
+        const std::uint64_t item = q < d.nitems ? d.items[q] : make_item(kItemEnd, 0, 0);
+        post_item(c, seq, item);
+        if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
+        const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
+        const Task task = p.tasks[static_cast<std::uint32_t>(item)];
+        produce_gemm_tile(p, c, task, cb * kBN, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
+          if (sg.bbuf == kBufWp) return;  // Wp is complete: permute_in ran before this launch
+          spin_until((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
+                     d.node_tiles[sg.src] * kConsumerWarps);
+          // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        });
       }
     }
     return;
   }
 
-  // ---------------- consumers: 2 x 2 warps, interleaved 8 x 8 fragments
-  const int wm = warp & 1, wn = warp >> 1;
-  const int fr = lane >> 2, fk = lane & 3;
-  // Fragment addresses (shared window, bytes) relative to the stage base. A: swizzled
-  // 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile. Fragment i of warp (wm, wn)
-  // covers rows 8*(2i+wm) .. +7 and fragment j columns 8*(2j+wn) .. +7: interleaving
-  // spreads a ragged tile's live fragments evenly over the four warps.
-  std::uint32_t a_off[4][4], b_off[4][4];  // [k step][fragment]
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    const int k = ks * 4 + fk;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a_off[ks][i] = 8u * a_swz(k, (2 * i + wm) * 8 + fr);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b_off[ks][j] = kChunkBytes + (k * kBPitch + (2 * j + wn) * 8 + fr) * 8;
-  }
-  const std::uint32_t smem_base = smem_u32(smem);
+  const FragAddr fa = frag_addresses(warp & 1, warp >> 1, lane >> 2, lane & 3);
   std::uint32_t it = 0;
   for (std::uint32_t seq = 0;; ++seq) {
-    const int slot = seq % kTileRing;
-    mbar_wait(&tfull[slot], (seq / kTileRing) & 1);
-    const std::uint32_t t = tring[slot];
-    mbar_arrive(&tempty[slot]);
-    if (t >= ntiles) break;
-    const Task task = p.tasks[t / col_blocks];
-    const std::uint32_t c0 = (t % col_blocks) * kBN;
-    std::uint32_t nchunks = 0;
-    for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
-    // Warp-uniform trim of fragments outside the task's valid rows / the last column
-    // block: their DMMAs are skipped.
-    const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
-    const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
-    const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
-    const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
-    // uniformly, once per tile) to a K loop instantiated for their live fragment count.
-    if (live_j == 4) {
-      switch (live_i) {
-        case 4: consume_chunks<4, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
-        case 3: consume_chunks<3, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
-        case 2: consume_chunks<2, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
-        case 1: consume_chunks<1, 4>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
-        default: consume_chunks<0, 0>(acc, full, empty, smem_base, a_off, b_off, nchunks, it); break;
-      }
-    } else {
-      consume_chunks_pred(acc, full, empty, smem_base, a_off, b_off, nchunks, it, live_i, live_j);
-    }
-
-    // epilogue: every valid element of the tile is stored exactly once (zeros for empty tasks)
-    double* C = pick_buf(p, task.cbuf);
-    const std::uint64_t ldc = pick_ld(p, task.cbuf);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = (2 * i + wm) * 8 + fr;
-      if (row >= task.m) continue;
-      double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = (2 * j + wn) * 8 + 2 * fk;
-        if (col + 1 < static_cast<int>(ncols))
-          *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-        else if (col < static_cast<int>(ncols))
-          crow[col] = acc[i][j][0];
-      }
-    }
+    const std::uint64_t item = take_item(c, seq);
+    if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
+    const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
+    const Task task = p.tasks[static_cast<std::uint32_t>(item)];
+    consume_gemm_tile(p, c, task, cb * kBN, fa, it);
+    if (task.cbuf != kBufYp)  // leaf rows (Yp) have no dependent inside the launch
+      warp_signal((task.cbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(task.node) * d.ncb + cb);
   }
 }
 

@@ -158,14 +158,19 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   plan.skel_rows = std::max<std::uint64_t>(rows, kRowAlign);
 
   const std::uint32_t bm = tile_m;
+  plan.node_tiles.assign(nn, 0);
+  std::uint32_t cur_node = 0;
   auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs, Phase& ph) {
     const std::uint32_t tiles = m == 0 ? 0 : (m + bm - 1) / bm;
+    if (cbuf != kBufYp) plan.node_tiles[cur_node] = tiles;
+    else plan.leaf_tasks += tiles;
     for (std::uint32_t t = 0; t < tiles; ++t) {
       const std::uint32_t r0 = t * bm;
       Task task{};
       task.c_row = static_cast<std::uint32_t>(c_row + r0);
       task.cbuf = cbuf;
       task.m = static_cast<std::uint16_t>(std::min(bm, m - r0));
+      task.node = cur_node;
       task.seg_begin = static_cast<std::uint32_t>(plan.segs.size());
       emit_segs(r0, task.m);
       task.seg_end = static_cast<std::uint32_t>(plan.segs.size());
@@ -182,7 +187,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   };
   // A operand rows [r0, r0+m) of the generator block at a_off; K columns; B rows b_row.
   auto push_seg = [&](Gen gen, bool trans, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k,
-                      std::uint32_t m, Buf bbuf, std::uint64_t b_row) {
+                      std::uint32_t m, Buf bbuf, std::uint64_t b_row, std::uint32_t src = 0) {
     if (k == 0) return;
     const std::uint64_t chunks = (k + kRowAlign - 1) / kRowAlign;
     TileSrc ts{};
@@ -195,7 +200,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     ts.trans = trans ? 1 : 0;
     for (std::uint64_t c = 0; c < chunks; ++c) plan.chunk_seg.push_back(static_cast<std::uint32_t>(plan.segs.size()));
     plan.segs.push_back(SegDev{plan.tile_elems, static_cast<std::uint32_t>(b_row),
-                               static_cast<std::uint16_t>(chunks), static_cast<std::uint16_t>(bbuf)});
+                               static_cast<std::uint16_t>(chunks), static_cast<std::uint16_t>(bbuf), src, 0});
     plan.tile_src.push_back(ts);
     plan.tile_elems += chunks * kRowAlign * bm;
   };
@@ -217,15 +222,18 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       if (sub_h[i] != h || !active(i)) continue;
       const std::uint64_t lda = v_width(i);
       const std::uint64_t vo = v.vptr[vslot[i]];
+      cur_node = i;
       add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
         if (is_leaf(i)) {
           push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, lda, m, kBufWp, plan.leaf_row[i]);
         } else {
           const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
           const std::uint64_t srl = v.sranks[lc];
-          if (active(lc)) push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc]);
+          if (active(lc))
+            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc], lc);
           if (active(rc))
-            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT, plan.node_off[rc]);
+            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT, plan.node_off[rc],
+                     rc);
         }
       }, plan.phases.back());
     }
@@ -239,15 +247,16 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     for (std::uint32_t c : order) {
       if (v.level[c] != d || !active(c)) continue;
       const std::uint32_t p = v.parent[c];
+      cur_node = c;
       add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0, std::uint32_t m) {
         for (std::uint64_t s : far_of[c]) {
           const std::uint32_t j = v.far_pairs[2 * s + 1];
-          push_seg(kGenB, false, v.bptr[s] + r0, v.sranks[c], v.sranks[j], m, kBufT, plan.node_off[j]);
+          push_seg(kGenB, false, v.bptr[s] + r0, v.sranks[c], v.sranks[j], m, kBufT, plan.node_off[j], j);
         }
         if (p != HMXG_NO_NODE && active(p)) {
           const std::uint64_t row_in_parent = (c == v.lchild[p]) ? 0 : v.sranks[v.lchild[p]];
           push_seg(kGenV, false, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], m, kBufS,
-                   plan.node_off[p]);
+                   plan.node_off[p], p);
         }
       }, plan.phases.back());
     }
@@ -259,8 +268,9 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   for (std::uint32_t i : order) {
     if (!is_leaf(i)) continue;
     const std::uint32_t m = size_of(i);
+    cur_node = i;
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
-      if (active(i)) push_seg(kGenV, false, v.vptr[vslot[i]] + r0, m, v.sranks[i], mt, kBufS, plan.node_off[i]);
+      if (active(i)) push_seg(kGenV, false, v.vptr[vslot[i]] + r0, m, v.sranks[i], mt, kBufS, plan.node_off[i], i);
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
         push_seg(kGenD, false, v.dptr[s] + r0, m, size_of(j), mt, kBufWp, plan.leaf_row[j]);

@@ -54,23 +54,30 @@ static_assert(sizeof(TileSrc) == 32, "TileSrc layout");
 
 // One K segment of a task as the GEMM kernel sees it: nchunks pre-tiled A chunks at
 // tile_off, and B rows [b_row, b_row + 16*nchunks) of buffer bbuf.
+// `src` is the node whose T or S rows the segment reads (the DAG kernel waits for that
+// node's tiles of the same column block); unused for Wp.
 struct SegDev {
   std::uint64_t tile_off;
   std::uint32_t b_row;
   std::uint16_t nchunks;
   std::uint16_t bbuf;
+  std::uint32_t src;
+  std::uint32_t pad;
 };
-static_assert(sizeof(SegDev) == 16, "SegDev layout");
+static_assert(sizeof(SegDev) == 24, "SegDev layout");
 
 // One output row tile: rows [c_row, c_row + m) of buffer cbuf, all columns (grid.y).
+// `node` owns the output rows (T or S of that node; Yp for a leaf).
 struct Task {
   std::uint32_t c_row;
   std::uint16_t cbuf;
   std::uint16_t m;
   std::uint32_t seg_begin;
   std::uint32_t seg_end;
+  std::uint32_t node;
+  std::uint32_t pad;
 };
-static_assert(sizeof(Task) == 16, "Task layout");
+static_assert(sizeof(Task) == 24, "Task layout");
 
 enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2 };
 
@@ -98,6 +105,8 @@ struct Plan {
   std::vector<std::uint32_t> chunk_seg; // pre-tiled chunk -> segment
   std::uint64_t tile_elems = 0;
   std::vector<Phase> phases;
+  std::vector<std::uint32_t> node_tiles;  // row tiles of each active node's T (= of its S)
+  std::uint32_t leaf_tasks = 0;           // row tiles of the leaf (Yp) phase
   std::uint64_t d_elems = 0, b_elems = 0, v_elems = 0;
   std::uint32_t max_m = 0;
 };

@@ -164,11 +164,11 @@ class Evaluator:
         return out
 
     def evaluate_host_ptr(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
-                          time_phases: bool = False, stats: EvalStats | None = None) -> None:
+                          time_phases: bool = False, stats: EvalStats | None = None, levels: bool = False) -> None:
         """Host-pointer evaluation (pinned buffers give overlapped PCIe transfers)."""
         n = self.cds.n
         st = N.Stats()
-        flags = N.HMXG_F_TIME_PHASES if time_phases else 0
+        flags = (N.HMXG_F_TIME_PHASES if time_phases else 0) | (N.HMXG_F_LEVEL_LAUNCHES if levels else 0)
         _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
                                       flags, None, C.byref(st)))
         if stats is not None:
@@ -176,8 +176,10 @@ class Evaluator:
             stats.device_ms = float(st.device_ms)
             stats.launches = int(st.launches)
 
-    def evaluate(self, w: np.ndarray, stats: EvalStats | None = None, out: np.ndarray | None = None) -> np.ndarray:
-        """Y = K~ W with host arrays (column major, float64)."""
+    def evaluate(self, w: np.ndarray, stats: EvalStats | None = None, out: np.ndarray | None = None,
+                 levels: bool = False) -> np.ndarray:
+        """Y = K~ W with host arrays (column major, float64). ``levels`` runs the
+        level-by-level launch sequence instead of the whole-evaluation DAG launch."""
         if w.ndim != 2:
             raise ValueError("evaluate: W must be a 2-D matrix")
         n, q = w.shape
@@ -190,7 +192,8 @@ class Evaluator:
         st = N.Stats()
         if q:
             _check(N.hmxg().hmxg_evaluate(self._h, wf.ctypes.data_as(C.c_void_p), n, q, n,
-                                          y.ctypes.data_as(C.c_void_p), n, 0, None, C.byref(st)))
+                                          y.ctypes.data_as(C.c_void_p), n,
+                                          N.HMXG_F_LEVEL_LAUNCHES if levels else 0, None, C.byref(st)))
         if stats is not None:
             stats.locked_pairs = int(st.locked_pairs)
             stats.seconds = float(st.seconds)
@@ -200,12 +203,12 @@ class Evaluator:
 
     def evaluate_device(self, w_ptr: int, y_ptr: int, q: int, ldw: int | None = None, ldy: int | None = None,
                         stream: int = 0, sync: bool = False, stats: EvalStats | None = None,
-                        time_phases: bool = False, graph: bool = True) -> None:
+                        time_phases: bool = False, graph: bool = True, levels: bool = False) -> None:
         """Device-pointer evaluation (single-device context): W/Y already in HBM,
         enqueued on ``stream`` (a cudaStream_t as int, 0 = internal stream)."""
         n = self.cds.n
         flags = (N.HMXG_F_DEVICE_PTRS | (0 if sync else N.HMXG_F_NO_SYNC) | (N.HMXG_F_TIME_PHASES if time_phases else 0)
-                 | (0 if graph else N.HMXG_F_NO_GRAPH))
+                 | (0 if graph else N.HMXG_F_NO_GRAPH) | (N.HMXG_F_LEVEL_LAUNCHES if levels else 0))
         st = N.Stats()
         _check(N.hmxg().hmxg_evaluate(self._h, C.c_void_p(w_ptr), n, q, ldw or n, C.c_void_p(y_ptr), ldy or n,
                                       flags, C.c_void_p(stream) if stream else None, C.byref(st)))

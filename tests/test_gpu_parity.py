@@ -179,3 +179,17 @@ def test_configs_full_size_column_subset(name):
     assert oracle.rel_frob(y2[:, 0], 3.0 * y[:, cols[0]] + y[:, cols[1]]) <= TOL
     ev.close()
     inst.close()
+
+
+@pytest.mark.parametrize("name,q", [("cfg1-hss", 64), ("cfg2-h2b", 200), ("cfg5-hss", 130)])
+def test_dag_launch_equals_level_launches(name, q):
+    """The whole-evaluation DAG launch (default) and the level-by-level launch sequence
+    compute every tile identically: bit-identical Y."""
+    spec, _ = config(name)
+    inst = build_instance(spec)
+    ev = Evaluator(inst.cds)
+    w = _w(inst.cds.n, q, 21)
+    a = ev.evaluate(w)
+    b = ev.evaluate(w, levels=True)
+    assert np.array_equal(a, b)
+    assert oracle.rel_frob(a, oracle.oracle_evaluate(inst.cds, w)) <= TOL

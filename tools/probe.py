@@ -26,10 +26,16 @@ for name in sys.argv[1:] or ["cfg1-hss", "cfg5-hss"]:
         ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream)
     e1.record(s); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream, time_phases=True)
+    e0.record(s)
+    for _ in range(reps):
+        ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream, levels=True)
+    e1.record(s); torch.cuda.synchronize()
+    ms_lv = e0.elapsed_time(e1) / reps
+    ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream, time_phases=True, levels=True, graph=False)
     torch.cuda.synchronize()
     fl, by = c.flops(q), c.bytes(q)
-    print(f"{name}: q={q} {ms:.3f} ms {fl/ms/1e9:.2f} TFLOP/s eval-roofline frac={max(fl/PEAK, by/6555.8e9)*1e3/ms:.3f}")
+    print(f"{name}: q={q} DAG {ms:.3f} ms {fl/ms/1e9:.2f} TFLOP/s eval-roofline frac={max(fl/PEAK, by/6555.8e9)*1e3/ms:.3f}"
+          f" | level launches {ms_lv:.3f} ms")
     for p in ev.phases():
         f = p["flops_per_col"] * q
         print(f"   {p['kind']:>13} L{p['level']:<2} tiles={p['tiles']:>6} {p['ms']:.4f} ms {f/max(p['ms'],1e-9)/1e9:7.2f} TF/s")
