@@ -222,14 +222,20 @@ def ours(args) -> None:
     import torch.distributed as dist
 
     from paper_1812_07152_b200 import EvalStats, Evaluator, build_instance, config
+    from paper_1812_07152_b200.distributed import column_shard
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.device is not None:  # testing the N>1 path on fewer GPUs (ranks share a device)
+        local = args.device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     def barrier():
         if world > 1:
@@ -238,7 +244,7 @@ def ours(args) -> None:
     def allmax(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -250,7 +256,7 @@ def ours(args) -> None:
     cds = inst.cds
     log(f"[rank {rank}] built {args.config} in {time.time() - t0:.1f}s: near={cds.num_near} far={cds.num_far} "
         f"|D|={cds.d_elems} |B|={cds.b_elems} |V|={cds.v_elems}")
-    c0, c1 = q_total * rank // world, q_total * (rank + 1) // world
+    c0, c1 = column_shard(q_total, world, rank)
     q = c1 - c0
     ev = Evaluator(cds, devices=(local,))
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -413,6 +419,9 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=1)
     ap.add_argument("--ref-warmup", type=int, default=0)
     ap.add_argument("--ref-cols", type=int, default=0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + --device: exercise the N>1 path with ranks sharing one GPU (testing only)")
+    ap.add_argument("--device", type=int, default=None, help="override LOCAL_RANK's device (testing only)")
     args = ap.parse_args()
     if args.impl == "reference-child":
         args.ref_step_s = args.ref_step_s
