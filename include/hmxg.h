@@ -140,6 +140,26 @@ int hmxg_free(hmxg_mat* mat);
 int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info);
 int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info);
 
+/* Subtree-split fallback for a CDS larger than one GPU's HBM. Part `part` of
+ * `nparts` (one single-device context per part, e.g. one rank per GPU) owns the subtrees
+ * below the top ceil(log2 nparts) tree levels assigned to it and holds only the
+ * generators its tiles read; W and Y are full-size on every part. Evaluation is two
+ * stages around an exchange of the skeleton weights T:
+ *   hmxg_split_stage(mat, 0, ...)  permute-in + upward pass over the part's subtrees
+ *   -- sum the parts' T buffers (hmxg_split_exchange_buffer; e.g. ncclAllReduce, sum) --
+ *   hmxg_split_stage(mat, 1, ...)  replicated top levels, far+downward and near/leaf for
+ *                                  the part's targets, permute-out
+ *   -- sum the parts' Y (rows of other parts are zero) --
+ * W / Y are device pointers on the part's device; each call returns when its stage is
+ * complete on `stream` (NULL = internal stream). */
+int hmxg_upload_split(hmxg_ctx* ctx, const hmxg_cds_view* cds, uint32_t nparts, uint32_t part, hmxg_mat** out);
+int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t q, size_t ldw, double* Y,
+                     size_t ldy, void* stream);
+int hmxg_split_exchange_buffer(hmxg_mat* mat, double** ptr, size_t* count);
+/* Copy the T exchange buffer (count = skel rows x row pitch doubles, see _buffer) to a
+ * device buffer (to_matrix = 0) or back into the matrix (to_matrix = 1). */
+int hmxg_split_exchange(hmxg_mat* mat, double* buf, size_t count, int to_matrix, void* stream);
+
 /* Y = K~ W. W is n x q column major with leading dimension ldw >= n, Y likewise.
  * Host pointers (default): columns are sharded over the context's devices, copied in,
  * evaluated and copied back; returns when Y is complete.

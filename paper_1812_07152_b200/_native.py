@@ -169,6 +169,11 @@ HMXG_SYMBOLS = {
         [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_size_t,
          C.c_uint, C.c_void_p, C.POINTER(Stats)],
     ),
+    "hmxg_upload_split": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "hmxg_split_stage": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p,
+                                   C.c_size_t, C.c_void_p]),
+    "hmxg_split_exchange_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "hmxg_split_exchange": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "hmxg_phase_count": (C.c_int, [C.c_void_p]),
     "hmxg_phase_get": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(Phase)]),
     "hmxg_last_error": (C.c_char_p, []),

@@ -117,12 +117,14 @@ struct DevState {
     std::size_t q = 0;
     std::uint64_t* items = nullptr;
     std::uint32_t nitems = 0;
+    std::uint32_t stage = 0;
   };
-  DagItems dag[3];                    // item lists of the last few column counts
+  DagItems dag[4];                    // item lists of the last few (column count, stage) keys
   std::uint32_t dag_next = 0;
   std::uint32_t* dag_done = nullptr;  // claim counter + done counters (sized for the largest q)
   std::size_t dag_done_cap = 0;
   std::uint32_t* node_tiles = nullptr;
+  std::uint32_t* remote_t = nullptr;  // split mode: nodes whose T comes from the exchange
   // CUDA graph of the whole launch sequence for one (W, Y, q, ld, stream, workspace) key:
   // repeated device-pointer evaluations replay it instead of issuing ~2H+4 launches.
   struct GraphKey {
@@ -179,6 +181,8 @@ struct DevState {
     }
     cudaFree(dag_done);
     cudaFree(node_tiles);
+    cudaFree(remote_t);
+    remote_t = nullptr;
     dag_done = nullptr;
     dag_done_cap = 0;
     node_tiles = nullptr;
@@ -249,32 +253,36 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 // levels in launch order (upward by height, far+downward by depth, leaves), each level's
 // row tiles in task order with the column block fastest (so a row tile's A chunks are
 // re-served from L2 to all column blocks).
-std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q) {
+std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
   std::vector<std::uint64_t> items;
   for (const Phase& ph : plan.phases)
+    if (ph.stage == stage)
     for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
       for (std::uint32_t cb = 0; cb < ncb; ++cb) items.push_back(make_item(kItemGemm, cb, t));
   return items;
 }
 
+// [claim counter per stage | T counters (nodes x ncb) | S counters (nodes x ncb)]
+constexpr std::size_t kDagClaimWords = 2;
 std::size_t dag_done_words(const Plan& plan, std::size_t q) {
   const std::size_t ncb = (q + kBN - 1) / kBN;
-  return 1 + 2 * std::size_t(plan.num_nodes) * ncb;
+  return kDagClaimWords + 2 * std::size_t(plan.num_nodes) * ncb;
 }
 
 // Item list and counters for q columns (built on first use, cached for a few q).
-int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, const DevState::DagItems** out) {
+int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, const DevState::DagItems** out,
+               std::uint32_t stage = 0) {
   for (const auto& e : d.dag)
-    if (e.items && e.q == q) {
+    if (e.items && e.q == q && e.stage == stage) {
       *out = &e;
       return HMXG_OK;
     }
-  DevState::DagItems& e = d.dag[d.dag_next++ % 3];
+  DevState::DagItems& e = d.dag[d.dag_next++ % 4];
   HMXG_CUDA(cudaStreamSynchronize(st));  // the slot's previous list may still be in use
   cudaFree(e.items);
   e = DevState::DagItems{};
-  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q));
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage);
   if (items.size() >= 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many work items");
   HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
   const std::size_t words = dag_done_words(plan, q);
@@ -287,6 +295,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   HMXG_CUDA(cudaStreamSynchronize(st));
   e.nitems = static_cast<std::uint32_t>(items.size());
   e.q = q;
+  e.stage = stage;
   *out = &e;
   return HMXG_OK;
 }
@@ -330,13 +339,13 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   if (!levels) {
     const DevState::DagItems* di = nullptr;
     for (const auto& e : d.dag)
-      if (e.items && e.q == q) di = &e;
+      if (e.items && e.q == q && e.stage == 0) di = &e;
     if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
     DagParams dp{};
     dp.items = di->items;
     dp.nitems = di->nitems;
     dp.claim = d.dag_done;
-    dp.done = d.dag_done + 1;
+    dp.done = d.dag_done + kDagClaimWords;
     dp.node_tiles = d.node_tiles;
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
@@ -435,6 +444,111 @@ int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size
 }  // namespace
 }  // namespace hmxg
 
+namespace hmxg {
+namespace {
+
+// Subtree-split upload: only the generator blocks this part's tiles read are copied to
+// the device (one compact array per generator kind); tile sources are re-based onto it.
+int compact_generators(const hmxg_cds_view& v, Plan& plan, const double* (&src)[3], std::vector<double> (&host)[3]) {
+  const std::uint64_t* ptr[3] = {v.dptr, v.bptr, v.vptr};
+  const std::uint64_t count[3] = {v.num_near, v.num_far, v.num_v};
+  const double* gen[3] = {v.dgen, v.bgen, v.vgen};
+  std::vector<std::uint64_t> base[3];
+  for (int g = 0; g < 3; ++g) base[g].assign(count[g], ~std::uint64_t(0));
+  for (TileSrc& ts : plan.tile_src) {
+    const int g = ts.gen;
+    const std::uint64_t slot = std::upper_bound(ptr[g], ptr[g] + count[g] + 1, ts.a_off) - ptr[g] - 1;
+    if (slot >= count[g]) return set_err(HMXG_EINVAL, "split upload: tile source outside its generator");
+    if (base[g][slot] == ~std::uint64_t(0)) {
+      base[g][slot] = host[g].size();
+      host[g].insert(host[g].end(), gen[g] + ptr[g][slot], gen[g] + ptr[g][slot + 1]);
+    }
+    ts.a_off = base[g][slot] + (ts.a_off - ptr[g][slot]);
+  }
+  for (int g = 0; g < 3; ++g) src[g] = host[g].data();
+  plan.d_elems = host[0].size();
+  plan.b_elems = host[1].size();
+  plan.v_elems = host[2].size();
+  return HMXG_OK;
+}
+
+int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split, hmxg_mat** out) {
+  if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
+  *out = nullptr;
+  auto mat = std::make_unique<hmxg_mat>();
+  mat->ctx = ctx;
+  std::string err;
+  if (!build_plan(*cds, kBM, mat->plan, err, split)) return set_err(HMXG_EINVAL, err);
+  const double* gsrc[3] = {cds->dgen, cds->bgen, cds->vgen};
+  std::vector<double> gcompact[3];
+  if (split.nparts > 1) HMXG_TRY(compact_generators(*cds, mat->plan, gsrc, gcompact));
+  const Plan& plan = mat->plan;
+  mat->devs.resize(ctx->devs.size());
+  for (std::size_t g = 0; g < ctx->devs.size(); ++g) {
+    DevState& d = mat->devs[g];
+    d.dev = ctx->devs[g];
+    HMXG_CUDA(cudaSetDevice(d.dev));
+    for (cudaStream_t* st : {&d.comp, &d.h2d, &d.d2h}) HMXG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&d.ev0, &d.ev1}) HMXG_CUDA(cudaEventCreate(e));
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
+        HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    d.phase_ev.resize(plan.phases.size() + 3);
+    for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
+    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_CUDA(cudaFuncSetAttribute(eval_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    {
+      int per_sm = 0, sms = 0;
+      int per_sm_dag = 0;
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dag, eval_dag, kThreads, kSmemBytes));
+      // eval_dag relies on every CTA of its grid being resident (items wait on earlier items)
+      per_sm = std::min(per_sm, per_sm_dag);
+      HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
+#ifndef HMXG_GEMM_CTAS_PER_SM
+#define HMXG_GEMM_CTAS_PER_SM 3
+#endif
+      d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
+      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size()) * sizeof(std::uint32_t)));
+    }
+    // raw generators -> pre-tiled A operands on the device, then the raw copies go away
+    double *gd = nullptr, *gb = nullptr, *gv = nullptr;
+    TileSrc* srcs = nullptr;
+    std::uint32_t* cseg = nullptr;
+    HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
+    HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
+    HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
+    HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
+    HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
+    if (plan.tile_elems) {
+      HMXG_CUDA(cudaMalloc(&d.tiles, plan.tile_elems * sizeof(double)));
+      const std::uint64_t nch = plan.chunk_seg.size();
+      tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
+                                                                                               d.tiles, nch);
+      HMXG_CUDA(cudaGetLastError());
+    }
+    HMXG_CUDA(cudaStreamSynchronize(d.comp));
+    cudaFree(gd);
+    cudaFree(gb);
+    cudaFree(gv);
+    cudaFree(srcs);
+    cudaFree(cseg);
+    HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
+    HMXG_CUDA(cudaStreamSynchronize(d.comp));
+    d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
+                       4 * plan.ipmap.size();
+  }
+  *out = mat.release();
+  return HMXG_OK;
+}
+
+}  // namespace
+}  // namespace hmxg
+
 using namespace hmxg;
 
 extern "C" {
@@ -489,73 +603,101 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
   return HMXG_OK;
 }
 
+
 int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
-  if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
-  *out = nullptr;
-  auto mat = std::make_unique<hmxg_mat>();
-  mat->ctx = ctx;
-  std::string err;
-  if (!build_plan(*cds, kBM, mat->plan, err)) return set_err(HMXG_EINVAL, err);
+  return upload_impl(ctx, cds, SplitSpec{}, out);
+}
+
+int hmxg_upload_split(hmxg_ctx* ctx, const hmxg_cds_view* cds, uint32_t nparts, uint32_t part, hmxg_mat** out) {
+  if (nparts == 0 || part >= nparts) return set_err(HMXG_EINVAL, "hmxg_upload_split: bad part / nparts");
+  if (ctx && ctx->devs.size() != 1) return set_err(HMXG_EINVAL, "hmxg_upload_split: one device per part");
+  return upload_impl(ctx, cds, SplitSpec{nparts, part}, out);
+}
+
+int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t q, size_t ldw, double* Y, size_t ldy,
+                     void* stream) {
+  if (!mat) return set_err(HMXG_EINVAL, "hmxg_split_stage: null matrix");
   const Plan& plan = mat->plan;
-  mat->devs.resize(ctx->devs.size());
-  for (std::size_t g = 0; g < ctx->devs.size(); ++g) {
-    DevState& d = mat->devs[g];
-    d.dev = ctx->devs[g];
-    HMXG_CUDA(cudaSetDevice(d.dev));
-    for (cudaStream_t* st : {&d.comp, &d.h2d, &d.d2h}) HMXG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&d.ev0, &d.ev1}) HMXG_CUDA(cudaEventCreate(e));
-    for (int b = 0; b < 2; ++b)
-      for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
-        HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    d.phase_ev.resize(plan.phases.size() + 3);
-    for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
-    HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    HMXG_CUDA(cudaFuncSetAttribute(eval_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    {
-      int per_sm = 0, sms = 0;
-      int per_sm_dag = 0;
-      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
-      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dag, eval_dag, kThreads, kSmemBytes));
-      // eval_dag relies on every CTA of its grid being resident (items wait on earlier items)
-      per_sm = std::min(per_sm, per_sm_dag);
-      HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
-#ifndef HMXG_GEMM_CTAS_PER_SM
-#define HMXG_GEMM_CTAS_PER_SM 3
-#endif
-      d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
-      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size()) * sizeof(std::uint32_t)));
-    }
-    // raw generators -> pre-tiled A operands on the device, then the raw copies go away
-    double *gd = nullptr, *gb = nullptr, *gv = nullptr;
-    TileSrc* srcs = nullptr;
-    std::uint32_t* cseg = nullptr;
-    HMXG_TRY(dev_upload(&gd, cds->dgen, plan.d_elems, d.comp));
-    HMXG_TRY(dev_upload(&gb, cds->bgen, plan.b_elems, d.comp));
-    HMXG_TRY(dev_upload(&gv, cds->vgen, plan.v_elems, d.comp));
-    HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
-    HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
-    if (plan.tile_elems) {
-      HMXG_CUDA(cudaMalloc(&d.tiles, plan.tile_elems * sizeof(double)));
-      const std::uint64_t nch = plan.chunk_seg.size();
-      tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
-                                                                                               d.tiles, nch);
-      HMXG_CUDA(cudaGetLastError());
-    }
-    HMXG_CUDA(cudaStreamSynchronize(d.comp));
-    cudaFree(gd);
-    cudaFree(gb);
-    cudaFree(gv);
-    cudaFree(srcs);
-    cudaFree(cseg);
-    HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
-    HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
-    HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
-    HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
-    HMXG_CUDA(cudaStreamSynchronize(d.comp));
-    d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
-                       4 * plan.ipmap.size();
+  if (n != plan.n) return set_err(HMXG_EINVAL, "evaluate: W row count does not match the point count");
+  if (q == 0) return HMXG_OK;
+  if (stage < 0 || stage > 1 || !W || !Y || ldw < n || ldy < n || mat->devs.size() != 1)
+    return set_err(HMXG_EINVAL, "hmxg_split_stage: bad arguments");
+  std::lock_guard<std::mutex> lock(mat->mu);
+  DevState& d = mat->devs[0];
+  HMXG_CUDA(cudaSetDevice(d.dev));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.comp;
+  HMXG_TRY(ensure_workspace(plan, d, q));
+  const DevState::DagItems* di = nullptr;
+  HMXG_TRY(ensure_dag(plan, d, q, st, &di, static_cast<std::uint32_t>(stage)));
+  const std::uint32_t qq = static_cast<std::uint32_t>(q), nn = static_cast<std::uint32_t>(n);
+  const std::uint64_t ldq = d.cap_q;
+  const std::uint32_t ncb = (qq + kBN - 1) / kBN;
+  CUtensorMap tm_wp, tm_t, tm_s;
+  HMXG_TRY(make_map(&tm_wp, d.wp, plan.rows_pad, q, ldq));
+  HMXG_TRY(make_map(&tm_t, d.t, plan.skel_rows, q, ldq));
+  HMXG_TRY(make_map(&tm_s, d.s, plan.skel_rows, q, ldq));
+  GemmParams p{};
+  p.tiles = d.tiles;
+  p.tasks = d.tasks;
+  p.segs = d.segs;
+  p.buf[kBufWp] = d.wp;
+  p.buf[kBufT] = d.t;
+  p.buf[kBufS] = d.s;
+  p.buf[kBufYp] = d.yp;
+  for (auto& l : p.ld) l = ldq;
+  p.q = qq;
+  DagParams dp{};
+  dp.items = di->items;
+  dp.nitems = di->nitems;
+  dp.claim = d.dag_done + stage;
+  dp.done = d.dag_done + kDagClaimWords;
+  dp.node_tiles = d.node_tiles;
+  dp.ncb = ncb;
+  dp.nodes = plan.num_nodes;
+  const dim3 pgrid((nn + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
+  if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_split_stage: too many columns for one call");
+  if (stage == 0) {
+    // T rows of other parts and of the top levels must be zero for the exchange (a sum);
+    // Y' rows of other parts' leaves stay zero so the parts' Y sum to the full Y
+    HMXG_CUDA(cudaMemsetAsync(d.t, 0, plan.skel_rows * ldq * sizeof(double), st));
+    HMXG_CUDA(cudaMemsetAsync(d.yp, 0, plan.rows_pad * ldq * sizeof(double), st));
+    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
+    permute_in<<<pgrid, 256, 0, st>>>(W, ldw, d.ipmap, d.wp, ldq, nn, qq);
+  } else if (!plan.remote_t_nodes.empty()) {
+    // T of the other parts' nodes arrived through the exchange: mark it complete
+    const std::uint64_t cells = std::uint64_t(plan.remote_t_nodes.size()) * ncb;
+    preset_done<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(
+        d.remote_t, static_cast<std::uint32_t>(plan.remote_t_nodes.size()), dp.done, ncb, d.node_tiles);
   }
-  *out = mat.release();
+  if (di->nitems) {
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
+    eval_dag<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+  }
+  if (stage == 1) permute_out<<<pgrid, 256, 0, st>>>(d.yp, ldq, d.ipmap, Y, ldy, nn, qq);
+  HMXG_CUDA(cudaGetLastError());
+  HMXG_CUDA(cudaStreamSynchronize(st));
+  return HMXG_OK;
+}
+
+int hmxg_split_exchange(hmxg_mat* mat, double* buf, size_t count, int to_matrix, void* stream) {
+  double* t = nullptr;
+  size_t need = 0;
+  HMXG_TRY(hmxg_split_exchange_buffer(mat, &t, &need));
+  if (!buf || count != need) return set_err(HMXG_EINVAL, "hmxg_split_exchange: buffer size mismatch");
+  DevState& d = mat->devs[0];
+  HMXG_CUDA(cudaSetDevice(d.dev));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.comp;
+  HMXG_CUDA(cudaMemcpyAsync(to_matrix ? t : buf, to_matrix ? buf : t, need * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  HMXG_CUDA(cudaStreamSynchronize(st));
+  return HMXG_OK;
+}
+
+int hmxg_split_exchange_buffer(hmxg_mat* mat, double** ptr, size_t* count) {
+  if (!mat || !ptr || !count || mat->devs.empty()) return set_err(HMXG_EINVAL, "hmxg_split_exchange_buffer: null");
+  DevState& d = mat->devs[0];
+  if (!d.t) return set_err(HMXG_EINVAL, "hmxg_split_exchange_buffer: run stage 0 first");
+  *ptr = d.t;
+  *count = mat->plan.skel_rows * d.cap_q;
   return HMXG_OK;
 }
 

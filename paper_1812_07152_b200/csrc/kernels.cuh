@@ -493,6 +493,16 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   }
 }
 
+// Subtree-split stage 1: the T tiles of the other parts' nodes were filled by the
+// exchange; mark them complete for every column block.
+__global__ void preset_done(const std::uint32_t* __restrict__ nodes, std::uint32_t count, std::uint32_t* done_t,
+                            std::uint32_t ncb, const std::uint32_t* __restrict__ node_tiles) {
+  const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<std::uint64_t>(count) * ncb) return;
+  const std::uint32_t node = nodes[i / ncb], cb = static_cast<std::uint32_t>(i % ncb);
+  done_t[static_cast<std::uint64_t>(node) * ncb + cb] = node_tiles[node] * kConsumerWarps;
+}
+
 // Transpose-permute into the point-major internal layout: Wp[ipmap[r], c] = W[r, c].
 // A 32 x 32 tile is read column by column (256 B contiguous per column of W), turned
 // around in shared memory and written row by row (256 B contiguous per point row of Wp),

@@ -21,7 +21,7 @@ bool fail(std::string& err, A&&... parts) {
 
 }  // namespace
 
-bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err) {
+bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err, const SplitSpec& split) {
   plan = Plan{};
   const std::uint32_t nn = v.num_nodes;
   if (nn == 0) return fail(err, "cds: empty tree");
@@ -159,11 +159,12 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
 
   const std::uint32_t bm = tile_m;
   plan.node_tiles.assign(nn, 0);
+  for (std::uint32_t i = 0; i < nn; ++i)
+    if (active(i)) plan.node_tiles[i] = (v.sranks[i] + bm - 1) / bm;
   std::uint32_t cur_node = 0;
   auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs, Phase& ph) {
     const std::uint32_t tiles = m == 0 ? 0 : (m + bm - 1) / bm;
-    if (cbuf != kBufYp) plan.node_tiles[cur_node] = tiles;
-    else plan.leaf_tasks += tiles;
+    if (cbuf == kBufYp) plan.leaf_tasks += tiles;
     for (std::uint32_t t = 0; t < tiles; ++t) {
       const std::uint32_t r0 = t * bm;
       Task task{};
@@ -204,8 +205,35 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     plan.tile_src.push_back(ts);
     plan.tile_elems += chunks * kRowAlign * bm;
   };
+  // --- subtree split: owner part of every node (-1: replicated top level)
+  if (split.nparts == 0 || split.part >= split.nparts) return fail(err, "split: bad part / nparts");
+  plan.nparts = split.nparts;
+  plan.part = split.part;
+  const bool splitting = split.nparts > 1;
+  std::vector<int> owner(nn, 0);
+  if (splitting) {
+    std::uint32_t top_depth = 0;
+    while ((1u << top_depth) < split.nparts) ++top_depth;
+    std::vector<std::uint32_t> roots;  // subtree roots in tree-position order
+    for (std::uint32_t i : order)
+      if (v.level[i] == top_depth || (v.level[i] < top_depth && is_leaf(i))) roots.push_back(i);
+    std::sort(roots.begin(), roots.end(), [&](std::uint32_t a, std::uint32_t b) { return v.start[a] < v.start[b]; });
+    for (std::uint32_t i = 0; i < nn; ++i) owner[i] = -1;
+    for (std::size_t k = 0; k < roots.size(); ++k)
+      owner[roots[k]] = static_cast<int>(k * split.nparts / roots.size());
+    for (std::uint32_t i : order)  // BFS: parents before children
+      if (!is_leaf(i) && owner[i] >= 0) owner[v.lchild[i]] = owner[v.rchild[i]] = owner[i];
+    for (std::uint32_t i = 0; i < nn; ++i)
+      if (owner[i] >= 0 && owner[i] != static_cast<int>(split.part) && active(i)) plan.remote_t_nodes.push_back(i);
+  }
+  const int me = static_cast<int>(split.part);
+  auto mine = [&](std::uint32_t i) { return !splitting || owner[i] == me; };
+  auto top = [&](std::uint32_t i) { return splitting && owner[i] < 0; };
+
+  std::uint32_t cur_stage = 0;
   auto open_phase = [&](PhaseKind kind, std::uint32_t level) {
-    plan.phases.push_back(Phase{kind, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0, 0.0, 0.0});
+    plan.phases.push_back(
+        Phase{kind, cur_stage, static_cast<std::uint32_t>(plan.tasks.size()), 0, level, 0.0, 0.0, 0.0});
   };
   auto close_phase = [&]() {
     Phase& ph = plan.phases.back();
@@ -216,36 +244,41 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   // --- upward, by subtree height: T_i = V_i^T * (leaf ? Wp_i : [T_lc; T_rc])
   std::uint32_t max_h = 0;
   for (std::uint32_t i = 0; i < nn; ++i) max_h = std::max(max_h, sub_h[i]);
-  for (std::uint32_t h = 0; h <= max_h; ++h) {
-    open_phase(kPhaseUp, h);
-    for (std::uint32_t i : order) {
-      if (sub_h[i] != h || !active(i)) continue;
-      const std::uint64_t lda = v_width(i);
-      const std::uint64_t vo = v.vptr[vslot[i]];
-      cur_node = i;
-      add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
-        if (is_leaf(i)) {
-          push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, lda, m, kBufWp, plan.leaf_row[i]);
-        } else {
-          const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
-          const std::uint64_t srl = v.sranks[lc];
-          if (active(lc))
-            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc], lc);
-          if (active(rc))
-            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT, plan.node_off[rc],
-                     rc);
-        }
-      }, plan.phases.back());
+  auto upward_pass = [&](auto&& take) {
+    for (std::uint32_t h = 0; h <= max_h; ++h) {
+      open_phase(kPhaseUp, h);
+      for (std::uint32_t i : order) {
+        if (sub_h[i] != h || !active(i) || !take(i)) continue;
+        const std::uint64_t lda = v_width(i);
+        const std::uint64_t vo = v.vptr[vslot[i]];
+        cur_node = i;
+        add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
+          if (is_leaf(i)) {
+            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, lda, m, kBufWp, plan.leaf_row[i]);
+          } else {
+            const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
+            const std::uint64_t srl = v.sranks[lc];
+            if (active(lc))
+              push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc], lc);
+            if (active(rc))
+              push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT,
+                       plan.node_off[rc], rc);
+          }
+        }, plan.phases.back());
+      }
+      close_phase();
     }
-    close_phase();
-  }
+  };
+  upward_pass(mine);  // stage 0 (everything, without a split)
+  cur_stage = splitting ? 1 : 0;
+  if (splitting) upward_pass(top);  // stage 1: replicated top levels from the exchanged T
 
   // --- downward with the far pass folded in, by depth:
   //     S_c = sum_{far (c,j)} B_cj T_j + V_p[rows of c] S_p
   for (std::uint32_t d = 0; d <= height; ++d) {
     open_phase(kPhaseDown, d);
     for (std::uint32_t c : order) {
-      if (v.level[c] != d || !active(c)) continue;
+      if (v.level[c] != d || !active(c) || !(mine(c) || top(c))) continue;
       const std::uint32_t p = v.parent[c];
       cur_node = c;
       add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0, std::uint32_t m) {
@@ -266,7 +299,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j (every leaf row written once)
   open_phase(kPhaseLeaf, 0);
   for (std::uint32_t i : order) {
-    if (!is_leaf(i)) continue;
+    if (!is_leaf(i) || !mine(i)) continue;
     const std::uint32_t m = size_of(i);
     cur_node = i;
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {

@@ -83,6 +83,7 @@ enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2 };
 
 struct Phase {
   PhaseKind kind;
+  std::uint32_t stage;      // 0, or 1 = after the skeleton exchange (subtree-split mode)
   std::uint32_t task_begin, task_end;
   std::uint32_t level;      // height (up) or depth (down)
   double flops_per_col;     // 2*sum(m*k) over the phase's tiles, algorithmic
@@ -106,6 +107,9 @@ struct Plan {
   std::uint64_t tile_elems = 0;
   std::vector<Phase> phases;
   std::vector<std::uint32_t> node_tiles;  // row tiles of each active node's T (= of its S)
+  // subtree-split mode (SURVEY §8e fallback): nodes whose T arrives through the exchange
+  std::uint32_t nparts = 1, part = 0;
+  std::vector<std::uint32_t> remote_t_nodes;
   std::uint32_t leaf_tasks = 0;           // row tiles of the leaf (Yp) phase
   std::uint64_t d_elems = 0, b_elems = 0, v_elems = 0;
   std::uint32_t max_m = 0;
@@ -113,6 +117,16 @@ struct Plan {
 
 // Validates the view (structure.hpp invariants the evaluator relies on) and lowers it.
 // Returns false with `err` set on a malformed view. `tile_m` is the kernel's row tile.
-bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err);
+// Subtree split: the nodes below the top ceil(log2 nparts) levels are divided
+// by subtree into nparts contiguous parts. Part `part` gets stage 0 = the upward pass over
+// its own subtrees; stage 1 = the replicated top levels (upward), far+downward for its own
+// and the top nodes, and the leaf/near rows of its own leaves. Between the stages the
+// parts exchange T (each holds only its own rows; the sum of the parts' T is the full T).
+struct SplitSpec {
+  std::uint32_t nparts = 1;
+  std::uint32_t part = 0;
+};
+bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err,
+                const SplitSpec& split = {});
 
 }  // namespace hmxg

@@ -12,6 +12,7 @@ import hashlib
 
 import numpy as np
 
+from . import _native as N
 from .cds import CDS
 
 
@@ -73,3 +74,94 @@ def gather_columns(y_local: np.ndarray, q_total: int) -> np.ndarray:
     for r, (a, b) in enumerate(widths):
         y[:, a:b] = parts[r][: b - a].numpy().T
     return y
+
+
+class SplitPart:
+    """One part of the subtree-split fallback (include/hmxg.h hmxg_upload_split).
+
+    For a CDS that does not fit one GPU: part ``part`` of ``nparts`` holds only the
+    generators of its own subtrees (plus the replicated top levels). An evaluation is
+    stage 0 (upward over its subtrees), a sum-exchange of the skeleton weights T between
+    the parts, stage 1 (top levels, far+downward, near/leaf for its targets), and a sum
+    of the parts' Y (each part's Y is zero outside its rows).
+    """
+
+    def __init__(self, cds: CDS, nparts: int, part: int, device: int = 0):
+        import ctypes as C
+
+        from .executor import Context, _check
+
+        self._C, self._check = C, _check
+        self.cds, self.nparts, self.part = cds, nparts, part
+        self.ctx = Context((device,))
+        h = C.c_void_p()
+        v = cds.view()
+        _check(N.hmxg().hmxg_upload_split(self.ctx.handle, C.byref(v), nparts, part, C.byref(h)))
+        self._h = h
+
+    def stage(self, stage: int, w_ptr: int, y_ptr: int, q: int, stream: int = 0) -> None:
+        C = self._C
+        n = self.cds.n
+        self._check(N.hmxg().hmxg_split_stage(self._h, stage, C.c_void_p(w_ptr), n, q, n, C.c_void_p(y_ptr), n,
+                                              C.c_void_p(stream) if stream else None))
+
+    def exchange_count(self) -> int:
+        C = self._C
+        p, c = C.c_void_p(), C.c_size_t()
+        self._check(N.hmxg().hmxg_split_exchange_buffer(self._h, C.byref(p), C.byref(c)))
+        return int(c.value)
+
+    def exchange(self, buf_ptr: int, count: int, to_matrix: bool, stream: int = 0) -> None:
+        C = self._C
+        self._check(N.hmxg().hmxg_split_exchange(self._h, C.c_void_p(buf_ptr), count, 1 if to_matrix else 0,
+                                                 C.c_void_p(stream) if stream else None))
+
+    def info(self) -> N.Info:
+        C = self._C
+        inf = N.Info()
+        self._check(N.hmxg().hmxg_info_get(self._h, C.byref(inf)))
+        return inf
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.hmxg().hmxg_free(self._h)
+            self._h = None
+        self.ctx.close()
+
+
+def split_evaluate(cds: CDS, w, parts: list["SplitPart"] | None = None, nparts: int = 2, group=None):
+    """Y = K~ W with the subtree-split fallback, W a CUDA tensor of shape (q, n) (= n x q
+    column major). In one process all parts run on W's device and the exchange is a
+    local sum; under torch.distributed (one part per rank, ``parts=[this rank's part]``)
+    the exchanges are all-reduce sums over NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    q = w.shape[0]
+    distributed = dist.is_initialized() and dist.get_world_size() > 1
+
+    def allreduce(x):
+        if not distributed:
+            return x
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(x, group=group)
+            return x
+        h = x.cpu()
+        dist.all_reduce(h, group=group)
+        return h.to(x.device)
+
+    if parts is None:
+        parts = [SplitPart(cds, nparts, k, w.device.index or 0) for k in range(nparts)]
+    ys = [torch.zeros_like(w) for _ in parts]
+    for part, y in zip(parts, ys):
+        part.stage(0, w.data_ptr(), y.data_ptr(), q)
+    count = parts[0].exchange_count()
+    ts = [torch.empty(count, dtype=torch.float64, device=w.device) for _ in parts]
+    for part, t in zip(parts, ts):
+        part.exchange(t.data_ptr(), count, to_matrix=False)
+    total = allreduce(torch.stack(ts).sum(0) if len(ts) > 1 else ts[0])
+    for part in parts:
+        part.exchange(total.data_ptr(), count, to_matrix=True)
+    for part, y in zip(parts, ys):
+        part.stage(1, w.data_ptr(), y.data_ptr(), q)
+    return allreduce(torch.stack(ys).sum(0) if len(ys) > 1 else ys[0])
