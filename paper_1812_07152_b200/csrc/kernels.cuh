@@ -65,16 +65,23 @@ __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned byte
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// Waits trap after ~2^26 suspended polls (seconds): a dependency or transaction-count bug
+// then surfaces as a CUDA error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred done;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
-      "@!done bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  std::uint32_t done = 0, polls = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++polls > (1u << 26)) __trap();
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
   asm volatile(
@@ -277,7 +284,7 @@ __device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const Cta
       const int stage = it % kStages;
       if (it >= kStages) mbar_wait(&c.empty[stage], ((it / kStages) - 1) & 1);
       unsigned char* st = c.stage + stage * kStageBytes;
-      mbar_expect_tx(&c.full[stage], kStageBytes);
+      mbar_expect_tx(&c.full[stage], kChunkBytes + kBTileBytes);
       bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
                &c.full[stage]);
       // coordinates: {column (inner, Q-contiguous), row}
@@ -430,9 +437,11 @@ __device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
 __device__ __forceinline__ void spin_until(const std::uint32_t* p, std::uint32_t target) {
   if (ld_acquire(p) >= target) return;
   unsigned ns = 32;
+  std::uint32_t polls = 0;
   while (ld_acquire(p) < target) {
     __nanosleep(ns);
     ns = min(ns * 2, 256u);
+    if (++polls > (1u << 24)) __trap();  // ~4 s: a missing dependency signal, not a slow tile
   }
 }
 // A consumer warp has stored its part of an item: publish it. __syncwarp orders the
