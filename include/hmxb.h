@@ -78,6 +78,9 @@ int hmxb_stats(const hmxb_instance* inst, hmxb_build_stats* stats);
 int hmxb_dense_rows(const hmxb_instance* inst, const uint32_t* rows, uint64_t nrows,
                     const double* W, uint64_t q, uint64_t ldw, double* out, uint64_t ldo);
 void hmxb_free(hmxb_instance* inst);
+/* The reference CLI's random right-hand side (proj/tools/hmx.cpp:117-122): uniform[-1, 1)
+ * from xoshiro256** seeded with splitmix64(seed ^ splitmix64(0x77a7)), column major. */
+void hmxb_random_w(uint64_t seed, uint64_t n, uint64_t q, double* out);
 const char* hmxb_last_error(void);
 
 #ifdef __cplusplus

@@ -10,7 +10,7 @@
  * POD view of raw arrays; nothing here knows about torch or C++ types.
  *
  * Status codes: 0 ok, 1 invalid argument, 2 CUDA error, 3 out of memory,
- * 4 NCCL/collective error. A thread-local message is kept for hmxg_last_error().
+ * 4 NCCL/collective error, 5 file I/O or format error (reference exit code 3, io_error). A thread-local message is kept for hmxg_last_error().
  */
 #ifndef HMXG_H_
 #define HMXG_H_
@@ -27,6 +27,7 @@ extern "C" {
 #define HMXG_ECUDA 2
 #define HMXG_ENOMEM 3
 #define HMXG_ECOMM 4
+#define HMXG_EIO 5
 
 #define HMXG_NO_NODE 0xffffffffu
 
@@ -173,6 +174,18 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
  * HMXG_F_TIME_PHASES evaluation before filling last_ms. */
 int hmxg_phase_count(const hmxg_mat* mat);
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out);
+
+/* The reference's on-disk CDS (`hmat.cds`, format CDS1 v1, written by `hmx inspect` /
+ * hmx::save_cds: /root/reference/proj/src/serial.cpp:160-211, 271-308). The file is
+ * memory-mapped; the view's generator pointers point into the mapping (not necessarily
+ * 8-byte aligned), valid until hmxg_cds_file_close. Truncated files, a bad tag or version
+ * and inconsistent offsets are refused with HMXG_EIO (hmxg_cds_file_error()). */
+typedef struct hmxg_cds_file hmxg_cds_file;
+int hmxg_cds_file_open(const char* path, hmxg_cds_file** out);
+int hmxg_cds_file_view(const hmxg_cds_file* file, hmxg_cds_view* view);
+int hmxg_cds_file_header(const hmxg_cds_file* file, uint32_t* dim, double* bacc, uint32_t* max_rank);
+void hmxg_cds_file_close(hmxg_cds_file* file);
+const char* hmxg_cds_file_error(void);
 
 const char* hmxg_last_error(void);
 const char* hmxg_version(void);

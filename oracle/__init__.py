@@ -63,6 +63,14 @@ def _ref_lib():
             "hmxr_cds_from_view": (C.c_int, [C.POINTER(N.CdsView), C.POINTER(vp)]),
             "hmxr_cds_free": (None, [vp]),
             "hmxr_cds_evaluate": (C.c_int, [vp, vp, u64, u64, vp, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+            "hmxr_save_cds": (C.c_int, [vp, C.c_char_p]),
+            "hmxr_cds_save": (C.c_int, [vp, C.c_char_p]),
+            "hmxr_load_cds": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+            "hmxr_cds_view": (C.c_int, [vp, C.POINTER(N.CdsView)]),
+            "hmxr_save_matrix": (C.c_int, [C.c_char_p, vp, u64, u64]),
+            "hmxr_load_matrix": (C.c_int, [C.c_char_p, vp, C.POINTER(u64), C.POINTER(u64)]),
+            "hmxr_mix64": (u64, [u64]),
+            "hmxr_rng_fill_pm1": (None, [u64, u64, vp]),
             "hmxr_last_error": (C.c_char_p, []),
             "hmxr_hardware_workers": (C.c_uint, []),
         }
@@ -177,6 +185,10 @@ class RefInstance:
                                                         wf.shape[1], C.byref(eps)))
         return eps.value
 
+    def save_cds(self, path: str) -> None:
+        """hmx::save_cds of the reference's own CDS (serial.cpp:271-277)."""
+        _ref_check(_ref_lib().hmxr_save_cds(self._h, os.fsencode(path)))
+
     def close(self):
         if self._h:
             self.cds._cache.clear()
@@ -191,14 +203,29 @@ class RefInstance:
 
 
 class RefCds:
-    """The reference ``evaluate`` over any CDS (rebuilt as an hmx::CDS from the view)."""
+    """The reference ``evaluate`` over any CDS (rebuilt as an hmx::CDS from the view), or
+    over a CDS the reference read from disk (``RefCds.load``, hmx::load_cds)."""
 
-    def __init__(self, cds: CDS):
-        h = C.c_void_p()
+    def __init__(self, cds: CDS | None):
+        self._h = C.c_void_p()
+        if cds is None:
+            return
         v = cds.view()
-        _ref_check(_ref_lib().hmxr_cds_from_view(C.byref(v), C.byref(h)))
-        self._h = h
+        _ref_check(_ref_lib().hmxr_cds_from_view(C.byref(v), C.byref(self._h)))
         self.n = cds.n
+
+    @classmethod
+    def load(cls, path: str) -> "RefCds":
+        rc = cls(None)
+        _ref_check(_ref_lib().hmxr_load_cds(os.fsencode(path), C.byref(rc._h)))
+        v = N.CdsView()
+        _ref_lib().hmxr_cds_view(rc._h, C.byref(v))
+        rc.cds = CDS.from_view(v, owner=rc)
+        rc.n = rc.cds.n
+        return rc
+
+    def save(self, path: str) -> None:
+        _ref_check(_ref_lib().hmxr_cds_save(self._h, os.fsencode(path)))
 
     def evaluate(self, w: np.ndarray, p: int = 1, plan_bits: int = 0) -> tuple[np.ndarray, float]:
         wf = np.asfortranarray(w, dtype=np.float64)
@@ -218,6 +245,32 @@ class RefCds:
             self.close()
         except Exception:
             pass
+
+
+def ref_save_matrix(path: str, m: np.ndarray) -> None:
+    """hmx::save_matrix (serial.cpp:279-285)."""
+    mf = np.asfortranarray(m, dtype=np.float64)
+    _ref_check(_ref_lib().hmxr_save_matrix(os.fsencode(path), mf.ctypes.data_as(C.c_void_p), mf.shape[0],
+                                           mf.shape[1]))
+
+
+def ref_load_matrix(path: str) -> np.ndarray:
+    """hmx::load_matrix (serial.cpp:287-297)."""
+    r, c = C.c_uint64(), C.c_uint64()
+    _ref_check(_ref_lib().hmxr_load_matrix(os.fsencode(path), None, C.byref(r), C.byref(c)))
+    out = np.zeros((r.value, c.value), dtype=np.float64, order="F")
+    _ref_check(_ref_lib().hmxr_load_matrix(os.fsencode(path), out.ctypes.data_as(C.c_void_p), C.byref(r),
+                                           C.byref(c)))
+    return out
+
+
+def ref_cli_random_w(n: int, q: int, seed: int) -> np.ndarray:
+    """random_w of the reference CLI (proj/tools/hmx.cpp:117-122) composed from the
+    reference's own mix64 and Rng (the tool itself needs the absent vendor libraries)."""
+    lib = _ref_lib()
+    out = np.zeros((n, q), dtype=np.float64, order="F")
+    lib.hmxr_rng_fill_pm1(lib.hmxr_mix64(seed ^ lib.hmxr_mix64(0x77A7)), n * q, out.ctypes.data_as(C.c_void_p))
+    return out
 
 
 def random_matrix(rows: int, cols: int, seed: int) -> np.ndarray:

@@ -14,6 +14,10 @@
 //   hmxr_dense_apply    hmx::dense_apply        (proj/src/executor.cpp:405-429)
 //   hmxr_cds_from_view  an hmx::CDS rebuilt from a hmxg_cds_view (for CDSs produced by
 //                       this repo's instance builder) so the reference can evaluate it.
+//   hmxr_save_cds       hmx::save_cds    (proj/src/serial.cpp:271-277) -> `hmat.cds`
+//   hmxr_load_cds       hmx::load_cds    (proj/src/serial.cpp:299-308)
+//   hmxr_save_matrix    hmx::save_matrix (proj/src/serial.cpp:279-285)
+//   hmxr_load_matrix    hmx::load_matrix (proj/src/serial.cpp:287-297)
 #include <chrono>
 #include <cstring>
 #include <exception>
@@ -29,6 +33,7 @@
 #include "hmx/points.hpp"
 #include "hmx/rng.hpp"
 #include "hmx/sampling.hpp"
+#include "hmx/serial.hpp"
 #include "hmx/structure.hpp"
 #include "hmx/tree.hpp"
 
@@ -330,6 +335,52 @@ int hmxr_cds_evaluate(void* cds, const double* w, std::uint64_t n, std::uint64_t
     if (out.data.size()) std::memcpy(y, out.data.data(), out.data.size() * sizeof(double));
     if (seconds) *seconds = st.seconds;
   });
+}
+
+int hmxr_save_cds(void* inst, const char* path) {
+  auto* in = static_cast<RefInstance*>(inst);
+  return guarded([&] { hmx::save_cds(path, in->cds); });
+}
+
+int hmxr_cds_save(void* cds, const char* path) {
+  return guarded([&] { hmx::save_cds(path, static_cast<ViewCds*>(cds)->cds); });
+}
+
+int hmxr_load_cds(const char* path, void** out) {
+  return guarded([&] {
+    auto vc = std::make_unique<ViewCds>();
+    vc->cds = hmx::load_cds(path);
+    flatten(vc->cds, vc->near_flat, vc->far_flat);
+    *out = vc.release();
+  });
+}
+
+int hmxr_cds_view(void* cds, hmxg_cds_view* v) {
+  auto* vc = static_cast<ViewCds*>(cds);
+  fill_view(vc->cds, vc->near_flat, vc->far_flat, v);
+  return 0;
+}
+
+int hmxr_save_matrix(const char* path, const double* data, std::uint64_t rows, std::uint64_t cols) {
+  return guarded([&] { hmx::save_matrix(path, to_dense(data, rows, cols)); });
+}
+
+// rows/cols of the file in *rows/*cols; data copied to out when out != nullptr
+int hmxr_load_matrix(const char* path, double* out, std::uint64_t* rows, std::uint64_t* cols) {
+  return guarded([&] {
+    const auto m = hmx::load_matrix(path);
+    *rows = m.rows;
+    *cols = m.cols;
+    if (out && m.data.size()) std::memcpy(out, m.data.data(), m.data.size() * sizeof(double));
+  });
+}
+
+// The reference RNG primitives, so the CLI's random W (hmx.cpp:117-122) can be pinned.
+std::uint64_t hmxr_mix64(std::uint64_t x) { return hmx::mix64(x); }
+
+void hmxr_rng_fill_pm1(std::uint64_t state_seed, std::uint64_t count, double* out) {
+  hmx::Rng rng(state_seed);
+  for (std::uint64_t i = 0; i < count; ++i) out[i] = rng.uniform() * 2.0 - 1.0;
 }
 
 unsigned hmxr_hardware_workers(void) { return hmx::default_worker_count(); }

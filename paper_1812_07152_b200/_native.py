@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 HMXG_PATH = os.environ.get("HMXG_LIBRARY") or os.path.join(_HERE, "libhmxg.so")  # override: A/B builds
 HMXB_PATH = os.path.join(_HERE, "libhmxb.so")
 
-HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM = 0, 1, 2, 3, 4
+HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM, HMXG_EIO = 0, 1, 2, 3, 4, 5
 HMXG_NO_NODE = 0xFFFFFFFF
 HMXG_F_DEVICE_PTRS = 0x1
 HMXG_F_NO_SYNC = 0x2
@@ -176,6 +176,12 @@ HMXG_SYMBOLS = {
     "hmxg_split_exchange": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "hmxg_phase_count": (C.c_int, [C.c_void_p]),
     "hmxg_phase_get": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(Phase)]),
+    "hmxg_cds_file_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "hmxg_cds_file_view": (C.c_int, [C.c_void_p, C.POINTER(CdsView)]),
+    "hmxg_cds_file_header": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_uint32)]),
+    "hmxg_cds_file_close": (None, [C.c_void_p]),
+    "hmxg_cds_file_error": (C.c_char_p, []),
     "hmxg_last_error": (C.c_char_p, []),
     "hmxg_version": (C.c_char_p, []),
 }
@@ -190,6 +196,7 @@ HMXB_SYMBOLS = {
         [C.c_void_p, _u32p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64],
     ),
     "hmxb_free": (None, [C.c_void_p]),
+    "hmxb_random_w": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]),
     "hmxb_last_error": (C.c_char_p, []),
 }
 

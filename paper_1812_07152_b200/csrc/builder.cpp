@@ -1118,4 +1118,9 @@ int hmxb_dense_rows(const hmxb_instance* inst, const uint32_t* rows, uint64_t nr
 
 void hmxb_free(hmxb_instance* inst) { delete inst; }
 
+void hmxb_random_w(uint64_t seed, uint64_t n, uint64_t q, double* out) {
+  hmxb::Xoshiro rng(hmxb::splitmix64(seed ^ hmxb::splitmix64(0x77a7ULL)));
+  for (uint64_t i = 0; i < n * q; ++i) out[i] = rng.uniform() * 2.0 - 1.0;
+}
+
 }  // extern "C"
