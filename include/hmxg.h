@@ -28,6 +28,7 @@ extern "C" {
 #define HMXG_ENOMEM 3
 #define HMXG_ECOMM 4
 #define HMXG_EIO 5
+#define HMXG_EGUARD 6 /* hmx::numeric_guard_error (dense error oracle beyond n = 16384) */
 
 #define HMXG_NO_NODE 0xffffffffu
 
@@ -186,6 +187,38 @@ int hmxg_cds_file_view(const hmxg_cds_file* file, hmxg_cds_view* view);
 int hmxg_cds_file_header(const hmxg_cds_file* file, uint32_t* dim, double* bacc, uint32_t* max_rank);
 void hmxg_cds_file_close(hmxg_cds_file* file);
 const char* hmxg_cds_file_error(void);
+
+/* ---- Exact kernel products: the GPU error oracle.
+ * dense_apply (/root/reference/proj/src/executor.cpp:405-429) and relative_error_vs
+ * (:431-476) on the device. Points are uploaded once (n x d, point major, as
+ * hmx::PointSet::coords); every kernel tile is generated on the fly from them:
+ *   gaussian     exp(-|x-y|^2 / (2 h h))       (kernel.cpp:35-45)
+ *   invdist      |x-y| == 0 ? 1 : 1/|x-y|      (kernel.cpp:46-47)
+ *   exponential  exp(-|x-y| * (1/h))           (the builder's kernel, hmxb.h)
+ * and multiplied into W by the evaluator's FP64 DMMA GEMM. */
+typedef struct hmxg_points hmxg_points;
+#define HMXG_KERNEL_GAUSSIAN 0
+#define HMXG_KERNEL_EXPONENTIAL 1
+#define HMXG_KERNEL_INVDIST 2
+#define HMXG_ERR_DENSE 0
+#define HMXG_ERR_SAMPLED 1
+int hmxg_points_upload(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, int32_t kernel, double h,
+                       hmxg_points** out);
+int hmxg_points_free(hmxg_points* pts);
+/* Y[i + c*ldy] = sum_j K(x_{rows[i]}, x_j) W[j + c*ldw] for i < nrows, c < q; rows is a
+ * host array, or NULL for every point in order (nrows must then be n: dense_apply).
+ * HMXG_F_DEVICE_PTRS: W and Y are device pointers (else host). */
+int hmxg_kernel_rows(hmxg_points* pts, const uint32_t* rows, uint64_t nrows, const double* W, size_t n, size_t q,
+                     size_t ldw, double* Y, size_t ldy, unsigned flags, void* stream, hmxg_stats* stats);
+/* The sampled-mode row choice of relative_error_vs (executor.cpp:446-451): min(n, 256)
+ * rows by a partial Fisher-Yates shuffle seeded with mix64(seed ^ mix64(0xe44a11)).
+ * Host only; returns the row count written to rows[] (capacity >= min(n, 256)). */
+uint64_t hmxg_sample_rows(uint64_t n, uint64_t seed, uint32_t* rows);
+/* relative_error_vs: ||Y_approx - K W||_F / ||K W||_F over every entry (HMXG_ERR_DENSE,
+ * n <= 16384 else HMXG_EGUARD) or over the sampled rows (HMXG_ERR_SAMPLED). q == 0
+ * gives 0. HMXG_F_DEVICE_PTRS: Y_approx and W are device pointers. */
+int hmxg_relative_error(hmxg_points* pts, const double* Y_approx, size_t ldya, const double* W, size_t n, size_t q,
+                        size_t ldw, int mode, uint64_t seed, unsigned flags, double* eps);
 
 const char* hmxg_last_error(void);
 const char* hmxg_version(void);

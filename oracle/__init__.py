@@ -69,6 +69,9 @@ def _ref_lib():
             "hmxr_cds_view": (C.c_int, [vp, C.POINTER(N.CdsView)]),
             "hmxr_save_matrix": (C.c_int, [C.c_char_p, vp, u64, u64]),
             "hmxr_load_matrix": (C.c_int, [C.c_char_p, vp, C.POINTER(u64), C.POINTER(u64)]),
+            "hmxr_relative_error_vs": (C.c_int, [vp, vp, vp, u64, u64, C.c_int32, u64, C.POINTER(C.c_double)]),
+            "hmxr_dense_apply_points": (C.c_int, [vp, u64, u64, C.c_int32, C.c_double, vp, u64, vp]),
+            "hmxr_sample_rows": (u64, [u64, u64, vp]),
             "hmxr_mix64": (u64, [u64]),
             "hmxr_rng_fill_pm1": (None, [u64, u64, vp]),
             "hmxr_last_error": (C.c_char_p, []),
@@ -81,11 +84,17 @@ def _ref_lib():
     return _libs["r"]
 
 
+class RefNumericGuardError(RuntimeError):
+    """hmx::numeric_guard_error raised inside the reference."""
+
+
 def _ref_check(rc: int) -> None:
     if rc:
         msg = _ref_lib().hmxr_last_error().decode()
         if rc == 1:
             raise ValueError(msg)
+        if rc == 6:
+            raise RefNumericGuardError(msg)
         raise RuntimeError(f"reference status {rc}: {msg}")
 
 
@@ -185,6 +194,21 @@ class RefInstance:
                                                         wf.shape[1], C.byref(eps)))
         return eps.value
 
+    def relative_error_vs(self, y_approx: np.ndarray, w: np.ndarray, mode: int, seed: int = 0) -> float:
+        """hmx::relative_error_vs with this instance's kernel and points (mode 0 dense, 1 sampled)."""
+        ya = np.asfortranarray(y_approx, dtype=np.float64)
+        wf = np.asfortranarray(w, dtype=np.float64)
+        eps = C.c_double()
+        _ref_check(_ref_lib().hmxr_relative_error_vs(self._h, ya.ctypes.data_as(C.c_void_p),
+                                                     wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1], mode,
+                                                     seed, C.byref(eps)))
+        return eps.value
+
+    def points(self) -> np.ndarray:
+        p, n, d = C.POINTER(C.c_double)(), C.c_uint64(), C.c_uint64()
+        _ref_lib().hmxr_points(self._h, C.byref(p), C.byref(n), C.byref(d))
+        return np.ctypeslib.as_array(p, shape=(n.value, d.value)).copy()
+
     def save_cds(self, path: str) -> None:
         """hmx::save_cds of the reference's own CDS (serial.cpp:271-277)."""
         _ref_check(_ref_lib().hmxr_save_cds(self._h, os.fsencode(path)))
@@ -245,6 +269,23 @@ class RefCds:
             self.close()
         except Exception:
             pass
+
+
+def ref_dense_apply(points: np.ndarray, kernel: int, h: float, w: np.ndarray) -> np.ndarray:
+    """hmx::dense_apply (executor.cpp:405-429) over any points; kernel 0 gaussian, 1 invdist."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    wf = np.asfortranarray(w, dtype=np.float64)
+    y = np.zeros(wf.shape, dtype=np.float64, order="F")
+    _ref_check(_ref_lib().hmxr_dense_apply_points(pts.ctypes.data_as(C.c_void_p), pts.shape[0], pts.shape[1], kernel,
+                                                  h, wf.ctypes.data_as(C.c_void_p), wf.shape[1],
+                                                  y.ctypes.data_as(C.c_void_p)))
+    return y
+
+
+def ref_sample_rows(n: int, seed: int) -> np.ndarray:
+    out = np.zeros(min(n, 256), dtype=np.uint32)
+    _ref_lib().hmxr_sample_rows(n, seed, out.ctypes.data_as(C.c_void_p))
+    return out
 
 
 def ref_save_matrix(path: str, m: np.ndarray) -> None:

@@ -18,7 +18,9 @@
 //   hmxr_load_cds       hmx::load_cds    (proj/src/serial.cpp:299-308)
 //   hmxr_save_matrix    hmx::save_matrix (proj/src/serial.cpp:279-285)
 //   hmxr_load_matrix    hmx::load_matrix (proj/src/serial.cpp:287-297)
+#include <algorithm>
 #include <chrono>
+#include <vector>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -373,6 +375,47 @@ int hmxr_load_matrix(const char* path, double* out, std::uint64_t* rows, std::ui
     *cols = m.cols;
     if (out && m.data.size()) std::memcpy(out, m.data.data(), m.data.size() * sizeof(double));
   });
+}
+
+// hmx::relative_error_vs (executor.cpp:431-476) of a given approximation, mode 0 dense /
+// 1 sampled; status 6 = numeric_guard_error.
+int hmxr_relative_error_vs(void* inst, const double* ya, const double* w, std::uint64_t n, std::uint64_t q,
+                           std::int32_t mode, std::uint64_t seed, double* eps) {
+  auto* in = static_cast<RefInstance*>(inst);
+  try {
+    *eps = hmx::relative_error_vs(to_dense(ya, n, q), in->kernel, in->pts, to_dense(w, n, q),
+                                  mode == 0 ? hmx::ErrorMode::Dense : hmx::ErrorMode::Sampled, seed);
+    return 0;
+  } catch (const hmx::numeric_guard_error& e) {
+    return fail(e, 6);
+  } catch (const std::exception& e) {
+    return fail(e, 5);
+  }
+}
+
+// hmx::dense_apply over any point set (kernel 0 gaussian(h), 1 inverse distance).
+int hmxr_dense_apply_points(const double* coords, std::uint64_t n, std::uint64_t d, std::int32_t kernel, double h,
+                            const double* w, std::uint64_t q, double* y) {
+  return guarded([&] {
+    hmx::PointSet pts;
+    pts.n = n;
+    pts.d = d;
+    pts.coords.assign(coords, coords + n * d);
+    const hmx::Kernel k = kernel == 1 ? hmx::Kernel::inverse_distance() : hmx::Kernel::gaussian(h);
+    const auto out = hmx::dense_apply(k, pts, to_dense(w, n, q));
+    if (out.data.size()) std::memcpy(y, out.data.data(), out.data.size() * sizeof(double));
+  });
+}
+
+// The sampled rows of relative_error_vs (executor.cpp:446-451) drawn with the reference Rng.
+std::uint64_t hmxr_sample_rows(std::uint64_t n, std::uint64_t seed, std::uint32_t* rows) {
+  const std::uint64_t nr = std::min<std::uint64_t>(n, 256);
+  std::vector<std::uint32_t> all(n);
+  for (std::uint64_t i = 0; i < n; ++i) all[i] = static_cast<std::uint32_t>(i);
+  hmx::Rng rng(hmx::mix64(seed ^ hmx::mix64(0xe44a11ULL)));
+  for (std::uint64_t i = 0; i < nr; ++i) std::swap(all[i], all[i + rng.below(n - i)]);
+  std::copy(all.begin(), all.begin() + nr, rows);
+  return nr;
 }
 
 // The reference RNG primitives, so the CLI's random W (hmx.cpp:117-122) can be pinned.

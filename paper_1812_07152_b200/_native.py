@@ -16,7 +16,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 HMXG_PATH = os.environ.get("HMXG_LIBRARY") or os.path.join(_HERE, "libhmxg.so")  # override: A/B builds
 HMXB_PATH = os.path.join(_HERE, "libhmxb.so")
 
-HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM, HMXG_EIO = 0, 1, 2, 3, 4, 5
+HMXG_OK, HMXG_EINVAL, HMXG_ECUDA, HMXG_ENOMEM, HMXG_ECOMM, HMXG_EIO, HMXG_EGUARD = 0, 1, 2, 3, 4, 5, 6
+HMXG_KERNEL_GAUSSIAN, HMXG_KERNEL_EXPONENTIAL, HMXG_KERNEL_INVDIST = 0, 1, 2
+HMXG_ERR_DENSE, HMXG_ERR_SAMPLED = 0, 1
 HMXG_NO_NODE = 0xFFFFFFFF
 HMXG_F_DEVICE_PTRS = 0x1
 HMXG_F_NO_SYNC = 0x2
@@ -182,6 +184,14 @@ HMXG_SYMBOLS = {
                                        C.POINTER(C.c_uint32)]),
     "hmxg_cds_file_close": (None, [C.c_void_p]),
     "hmxg_cds_file_error": (C.c_char_p, []),
+    "hmxg_points_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_double,
+                                     C.POINTER(C.c_void_p)]),
+    "hmxg_points_free": (C.c_int, [C.c_void_p]),
+    "hmxg_kernel_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_size_t, C.c_size_t,
+                                   C.c_size_t, C.c_void_p, C.c_size_t, C.c_uint, C.c_void_p, C.POINTER(Stats)]),
+    "hmxg_sample_rows": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_void_p]),
+    "hmxg_relative_error": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_size_t,
+                                      C.c_size_t, C.c_int, C.c_uint64, C.c_uint, C.POINTER(C.c_double)]),
     "hmxg_last_error": (C.c_char_p, []),
     "hmxg_version": (C.c_char_p, []),
 }

@@ -22,6 +22,9 @@
 #include "plan.hpp"
 
 namespace hmxg {
+// Internal linkage: every translation unit of libhmxg.so that launches these kernels
+// gets its own instantiation (no duplicate host stubs at link time).
+namespace {
 
 constexpr int kBM = 64;        // output rows per CTA tile
 constexpr int kBN = 64;        // output columns per CTA tile
@@ -556,4 +559,5 @@ __global__ void __launch_bounds__(256) permute_out(const double* __restrict__ yp
   }
 }
 
+}  // namespace
 }  // namespace hmxg
