@@ -3,6 +3,7 @@
     python -m paper_1812_07152_b200 eval --out DIR [--w W.bin | --q Q --seed S] [--y Y.bin]
     python -m paper_1812_07152_b200 inspect --n N --d D [--synth uniform] ... --out DIR
     python -m paper_1812_07152_b200 bench --out DIR --q-list 1 256 1024
+    python -m paper_1812_07152_b200 accuracy --n N --bacc-list 1e-2 1e-3 1e-5 --q Q
 
 ``eval`` is ``cmd_eval`` (hmx.cpp:141-155) on the GPU: it reads ``DIR/hmat.cds`` (written
 by the reference's ``hmx inspect`` or by ``inspect`` here), takes W from ``--w`` or the
@@ -11,10 +12,13 @@ B200 and writes ``--y``. ``plan.json`` is read when present (its lowering switch
 pick a CPU schedule, so the GPU result does not depend on it); the reference requires it.
 ``inspect`` runs this repo's native instance builder (not the reference inspector) and
 writes ``hmat.cds`` + ``plan.json``. ``bench`` times the evaluation of a stored CDS for
-each Q on the device (W/Y resident in HBM) and end to end (host buffers).
+each Q on the device (W/Y resident in HBM) and end to end (host buffers). ``accuracy`` is
+``cmd_accuracy`` (hmx.cpp:157-170, accuracy_sweep pipeline.cpp:256-287): per bacc it builds
+the CDS (this repo's builder), evaluates on the B200 and measures eps_f with the GPU error
+oracle (dense for n <= 16384, else 256 sampled rows), printing the reference's CSV.
 
 The common options of hmx.cpp:39-58 are accepted with the same names; exit codes follow
-hmx.cpp:12-16 (0 ok, 2 usage, 3 I/O, 1 other).
+hmx.cpp:12-16 (0 ok, 2 usage, 3 I/O, 5 numeric guard, 1 other).
 """
 from __future__ import annotations
 
@@ -25,7 +29,7 @@ import time
 
 import numpy as np
 
-EXIT_OK, EXIT_USAGE, EXIT_IO = 0, 2, 3
+EXIT_OK, EXIT_USAGE, EXIT_IO, EXIT_NUMERIC_GUARD = 0, 2, 3, 5
 
 
 class _Parser(argparse.ArgumentParser):
@@ -207,7 +211,45 @@ def cmd_bench(o) -> int:
     return EXIT_OK
 
 
+def cmd_accuracy(o) -> int:
+    from .accuracy import DevicePoints, ErrorMode, Kernel
+    from .executor import EvalStats, Evaluator
+    from .instance import build_instance
+    from .serial import random_w
+
+    t_start = time.perf_counter()
+    spec = _builder_spec(o)
+    _echo_config("accuracy", o, spec.n, spec.d)
+    kernel = Kernel(spec.kernel, spec.h)
+    mode = ErrorMode.DENSE if spec.n <= 16384 else ErrorMode.SAMPLED
+    w = random_w(spec.n, o.q, o.seed)
+    lines, p1_seconds, oracle_seconds, dp = ["bacc,eps_f,eval_seconds,p2_seconds"], 0.0, 0.0, None
+    for i, bacc in enumerate(o.bacc_list):
+        spec.tol = bacc
+        inst = build_instance(spec)
+        st = inst.stats
+        p1 = st["seconds_points"] + st["seconds_tree"] + st["seconds_interactions"] + st["seconds_sampling"]
+        if i == 0:
+            p1_seconds = p1
+            dp = DevicePoints(inst.points(), kernel, o.device)
+        ev = Evaluator(inst.cds, devices=(o.device,))
+        stats = EvalStats()
+        y = ev.evaluate(w, stats)
+        t0 = time.perf_counter()
+        eps = dp.relative_error_vs(y, w, mode, o.seed)
+        oracle_seconds += time.perf_counter() - t0
+        lines.append(f"{bacc:g},{eps:g},{stats.seconds:g},{st['seconds_total'] - p1:g}")
+        ev.close()
+        inst.close()
+    print("\n".join(lines))
+    print(f"# p1={p1_seconds:g}s oracle={oracle_seconds:g}s total={time.perf_counter() - t_start:g}s")
+    if dp is not None:
+        dp.close()
+    return EXIT_OK
+
+
 def main(argv=None) -> int:
+    from .accuracy import NumericGuardError
     from .serial import IoError
 
     app = _Parser(prog="hmx-b200", description="B200 evaluation of hierarchical kernel matrices")
@@ -222,6 +264,10 @@ def main(argv=None) -> int:
     p_bench = sub.add_parser("bench", help="device and end-to-end evaluation time per Q")
     _add_common(p_bench)
     p_bench.add_argument("--q-list", type=int, nargs="+", default=[1, 256, 1024, 2048])
+    p_acc = sub.add_parser("accuracy", help="bacc sweep with the GPU error oracle, CSV output")
+    _add_common(p_acc)
+    p_acc.add_argument("--bacc-list", type=float, nargs="+", default=[1e-2, 1e-3, 1e-5])
+    p_acc.add_argument("--q", type=int, default=16)
     try:
         o = app.parse_args(argv)
     except SystemExit as e:
@@ -230,10 +276,13 @@ def main(argv=None) -> int:
         app.print_usage(sys.stderr)
         return EXIT_USAGE
     try:
-        return {"eval": cmd_eval, "inspect": cmd_inspect, "bench": cmd_bench}[o.cmd](o)
+        return {"eval": cmd_eval, "inspect": cmd_inspect, "bench": cmd_bench, "accuracy": cmd_accuracy}[o.cmd](o)
     except IoError as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_IO
+    except NumericGuardError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_NUMERIC_GUARD
     except ValueError as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_USAGE

@@ -58,3 +58,15 @@ def test_cli_eval_row_mismatch(stored):
     d, _ = stored
     oracle.ref_save_matrix(str(d / "wbad.bin"), np.ones((10, 2)))
     assert cli.main(["eval", "--out", str(d), "--w", str(d / "wbad.bin")]) == cli.EXIT_USAGE
+
+
+def test_cli_accuracy_sweep(tmp_path, capsys):
+    rc = cli.main(["accuracy", "--synth", "uniform", "--n", "4096", "--d", "3", "--leaf", "128", "--max-rank", "64",
+                   "--kernel", "gaussian:0.5", "--bacc-list", "1e-2", "1e-5", "--q", "8", "--seed", "2"])
+    assert rc == 0
+    out = capsys.readouterr().out.splitlines()
+    i = out.index("bacc,eps_f,eval_seconds,p2_seconds")
+    rows = [line.split(",") for line in out[i + 1:i + 3]]
+    eps = [float(r[1]) for r in rows]
+    assert 0.0 < eps[1] < eps[0] < 1.0  # a tighter tolerance gives a smaller error
+    assert out[i + 3].startswith("# p1=")
