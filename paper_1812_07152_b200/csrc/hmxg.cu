@@ -20,10 +20,10 @@
 namespace hmxg {
 namespace {
 
-// The GEMM B operand: boxes of 16 rows x kBPitch columns of a point-major buffer (the
-// pitch keeps fragment loads conflict-free), zero fill past column q.
-int make_map(CUtensorMap* map, const double* base, std::uint64_t rows, std::uint64_t cols, std::uint64_t ld) {
-  return make_map_box(map, base, rows, cols, ld, kBPitch, kBK);
+// The GEMM B operand: boxes of 16 rows x kBPitch columns of a point-major buffer in the
+// column-block layout (phys_col), zero fill past the last block.
+int make_map(CUtensorMap* map, const double* base, std::uint64_t rows, std::uint64_t q, std::uint64_t ld) {
+  return make_map_box(map, base, rows, phys_cols(q), ld, kBPitch, kBK);
 }
 
 // Columns per pipeline chunk of the host-pointer path: H2D of chunk k+1 and D2H of chunk
@@ -41,7 +41,7 @@ struct DevState {
   Task* tasks = nullptr;
   SegDev* segs = nullptr;
   std::uint32_t* ipmap = nullptr;
-  std::size_t cap_q = 0;  // evaluation workspace capacity in columns (= row pitch of Wp/T/S/Yp)
+  std::size_t cap_q = 0;  // row pitch of Wp/T/S/Yp in physical columns (phys_cols of the capacity)
   double* wp = nullptr;
   double* yp = nullptr;
   double* t = nullptr;
@@ -154,10 +154,10 @@ struct hmxg_mat {
 namespace hmxg {
 namespace {
 
-// Wp/Yp/T/S are point-major with a row pitch of cap_q columns (a multiple of 8: 64-byte
-// aligned rows for TMA and the vectorized epilogue).
+// Wp/Yp/T/S are point-major with a row pitch of cap_q physical columns: the column blocks
+// of q columns at kCbPitch (phys_cols(q), a multiple of 16: 128-byte aligned rows).
 int ensure_workspace(const Plan& plan, DevState& d, std::size_t q) {
-  q = (q + 7) / 8 * 8;
+  q = phys_cols(q);
   if (q <= d.cap_q) return HMXG_OK;
   d.release_workspace();
   const std::size_t n = plan.rows_pad, r = plan.skel_rows;
@@ -169,6 +169,9 @@ int ensure_workspace(const Plan& plan, DevState& d, std::size_t q) {
   HMXG_CUDA(cudaMemset(d.wp, 0, n * q * sizeof(double)));
   HMXG_CUDA(cudaMemset(d.t, 0, r * q * sizeof(double)));
   HMXG_CUDA(cudaMemset(d.s, 0, r * q * sizeof(double)));
+  // cudaMemset runs on the legacy stream, which does not order the non-blocking streams
+  // the evaluation is enqueued on: finish it before any kernel can touch the buffers
+  HMXG_CUDA(cudaDeviceSynchronize());
   d.cap_q = q;
   return HMXG_OK;
 }
@@ -734,7 +737,8 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     if (!levels) HMXG_TRY(ensure_dag(plan, d, q, st ? st : d.comp, &di));
     const bool sync = !(flags & HMXG_F_NO_SYNC);
     if (sync) HMXG_CUDA(cudaEventRecord(d.ev0, st));
-    if (st == nullptr || (flags & HMXG_F_NO_GRAPH)) {
+    // the legacy / per-thread default streams cannot be captured: launch directly there
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread || (flags & HMXG_F_NO_GRAPH)) {
       HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &launches));
     } else {
       const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, levels};

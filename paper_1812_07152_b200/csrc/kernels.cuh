@@ -43,6 +43,17 @@ constexpr int kChunkBytes = kChunkElems * 8;         // 8 KB
 // pattern. The 4 extra columns are the next column block's (or TMA zero fill past Q).
 constexpr int kBPitch = kBN + 4;
 constexpr int kBTileBytes = kBPitch * kBK * 8;       // 8704 B
+// Column blocks of the point-major buffers Wp/T/S/Yp are kCbPitch = 80 columns apart: 64
+// columns of data and a 128-byte gap. A B tile (kBPitch = 68 columns) then reads 4 gap
+// columns instead of the first line of the next column block, whose item may be storing
+// to it at that moment: no TMA box shares a cache line with another item's stores.
+constexpr int kCbPitch = kBN + 16;
+__host__ __device__ __forceinline__ std::uint64_t phys_col(std::uint64_t c) {
+  return (c / kBN) * kCbPitch + (c % kBN);
+}
+__host__ __device__ __forceinline__ std::uint64_t phys_cols(std::uint64_t q) {
+  return (q + kBN - 1) / kBN * kCbPitch;
+}
 constexpr int kStageBytes = kChunkBytes + kBTileBytes;
 
 struct GemmParams {
@@ -152,31 +163,49 @@ __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__
   }
 }
 
+// A consumer thread hands a stage (or a work-item slot) back to the producer. The mbarrier
+// arrive does not wait for the thread's outstanding ld.shared to return their data, so
+// without the fence the producer could refill the stage under an in-flight fragment load
+// (measured on B200: with heavy concurrent LSU traffic on the SM, fragment loads returned
+// the next chunk's data). fence.acq_rel.cta retires them first.
+__device__ __forceinline__ void release_stage(std::uint64_t* empty) {
+  asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+  mbar_arrive(empty);
+}
+
+// Fragment addresses of a consumer warp (shared window, bytes, relative to a stage): A
+// fragment i of k step ks sits at a_base + ks*kAStepBytes + i*kFragStride, B fragment j at
+// b_base + ks*kBStepBytes + j*kFragStride, so two base registers and compile-time
+// immediates replace a 32-entry address table (see frag_addresses).
+constexpr std::uint32_t kAStepBytes = 4 * kBM * 8;       // 4 k rows of the A chunk
+constexpr std::uint32_t kBStepBytes = 4 * kBPitch * 8;   // 4 k rows of the B tile
+constexpr std::uint32_t kFragStride = 16 * 8;            // fragments 2i+wm are 16 rows / columns apart
+
 // One tile's K loop for a consumer warp: LI x LJ live 8 x 8 fragments (compile time).
 // Fragments of k step ks+1 are loaded while step ks multiplies (register double buffer).
 template <int LI, int LJ>
 __device__ __forceinline__ void consume_chunks(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
-                                               std::uint32_t smem_base, const std::uint32_t (&a_off)[4][4],
-                                               const std::uint32_t (&b_off)[4][4], std::uint32_t nchunks,
-                                               std::uint32_t& it) {
+                                               std::uint32_t smem_base, std::uint32_t a_base, std::uint32_t b_base,
+                                               std::uint32_t nchunks, std::uint32_t& it) {
   for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
     const int stage = it % kStages;
     mbar_wait(&full[stage], (it / kStages) & 1);
-    const std::uint32_t st = smem_base + stage * kStageBytes;
+    const std::uint32_t sa = smem_base + stage * kStageBytes + a_base;
+    const std::uint32_t sb = smem_base + stage * kStageBytes + b_base;
     if (LI > 0 && LJ > 0) {
       double af[2][4], bf[2][4];
 #pragma unroll
-      for (int i = 0; i < LI; ++i) af[0][i] = lds64(st + a_off[0][i]);
+      for (int i = 0; i < LI; ++i) af[0][i] = lds64(sa + i * kFragStride);
 #pragma unroll
-      for (int j = 0; j < LJ; ++j) bf[0][j] = lds64(st + b_off[0][j]);
+      for (int j = 0; j < LJ; ++j) bf[0][j] = lds64(sb + j * kFragStride);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const int cur = ks & 1;
         if (ks + 1 < 4) {
 #pragma unroll
-          for (int i = 0; i < LI; ++i) af[cur ^ 1][i] = lds64(st + a_off[ks + 1][i]);
+          for (int i = 0; i < LI; ++i) af[cur ^ 1][i] = lds64(sa + (ks + 1) * kAStepBytes + i * kFragStride);
 #pragma unroll
-          for (int j = 0; j < LJ; ++j) bf[cur ^ 1][j] = lds64(st + b_off[ks + 1][j]);
+          for (int j = 0; j < LJ; ++j) bf[cur ^ 1][j] = lds64(sb + (ks + 1) * kBStepBytes + j * kFragStride);
         }
 #pragma unroll
         for (int i = 0; i < LI; ++i)
@@ -184,33 +213,34 @@ __device__ __forceinline__ void consume_chunks(double (&acc)[4][4][2], std::uint
           for (int j = 0; j < LJ; ++j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
       }
     }
-    mbar_arrive(&empty[stage]);  // every consumer thread releases the stage after its last read
+    release_stage(&empty[stage]);  // every consumer thread releases the stage after its last read
   }
 }
 
 // Partial column block (Q not a multiple of 64): runtime-predicated fragments.
 __device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
-                                                 std::uint32_t smem_base, const std::uint32_t (&a_off)[4][4],
-                                                 const std::uint32_t (&b_off)[4][4], std::uint32_t nchunks,
-                                                 std::uint32_t& it, int live_i, int live_j) {
+                                                    std::uint32_t smem_base, std::uint32_t a_base,
+                                                    std::uint32_t b_base, std::uint32_t nchunks, std::uint32_t& it,
+                                                    int live_i, int live_j) {
   for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
     const int stage = it % kStages;
     mbar_wait(&full[stage], (it / kStages) & 1);
-    const std::uint32_t st = smem_base + stage * kStageBytes;
+    const std::uint32_t sa = smem_base + stage * kStageBytes + a_base;
+    const std::uint32_t sb = smem_base + stage * kStageBytes + b_base;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = i < live_i ? lds64(st + a_off[ks][i]) : 0.0;
+      for (int i = 0; i < 4; ++i) af[i] = i < live_i ? lds64(sa + ks * kAStepBytes + i * kFragStride) : 0.0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = j < live_j ? lds64(st + b_off[ks][j]) : 0.0;
+      for (int j = 0; j < 4; ++j) bf[j] = j < live_j ? lds64(sb + ks * kBStepBytes + j * kFragStride) : 0.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (i < live_i && j < live_j) dmma884(acc[i][j], af[i], bf[j]);
     }
-    mbar_arrive(&empty[stage]);
+    release_stage(&empty[stage]);
   }
 }
 
@@ -269,16 +299,18 @@ __device__ __forceinline__ std::uint64_t take_item(const CtaSmem& c, std::uint32
   const int slot = seq % kTileRing;
   mbar_wait(&c.tfull[slot], (seq / kTileRing) & 1);
   const std::uint64_t item = c.tring[slot];
-  mbar_arrive(&c.tempty[slot]);
+  release_stage(&c.tempty[slot]);  // the ld.shared of the slot must retire first
   return item;
 }
 
-// Producer lane: stream the A chunks and B tiles of one GEMM tile. `wait_dep(seg)` runs
-// before a segment's first load (the DAG kernel's dependency wait; a no-op per level).
+// Producer lane: stream the A chunks and B tiles of one GEMM tile (column block cb).
+// `wait_dep(seg)` runs before a segment's first load (the DAG kernel's dependency wait; a
+// no-op per level).
 template <class WaitDep>
 __device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
-                                                  std::uint32_t c0, const CUtensorMap* tm_wp, const CUtensorMap* tm_t,
+                                                  std::uint32_t cb, const CUtensorMap* tm_wp, const CUtensorMap* tm_t,
                                                   const CUtensorMap* tm_s, std::uint32_t& it, WaitDep&& wait_dep) {
+  const int x = static_cast<int>(cb * kCbPitch);
   for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
     const SegDev sg = p.segs[si];
     wait_dep(sg);
@@ -291,36 +323,33 @@ __device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const Cta
       bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
                &c.full[stage]);
       // coordinates: {column (inner, Q-contiguous), row}
-      tma_2d_g2s(st + kChunkBytes, map, static_cast<int>(c0), static_cast<int>(sg.b_row + ch * kBK),
-                 &c.full[stage]);
+      tma_2d_g2s(st + kChunkBytes, map, x, static_cast<int>(sg.b_row + ch * kBK), &c.full[stage]);
     }
   }
 }
 
-// Per-thread fragment address table of a consumer warp (shared window, bytes, relative to
-// a stage). A: swizzled 64 x 16 chunk; B: the 16 x kBPitch row-major TMA tile. Fragment
-// i of warp (wm, wn) covers rows 8*(2i+wm) .. +7 and fragment j columns 8*(2j+wn) .. +7:
-// interleaving spreads a ragged tile's live fragments evenly over the four warps.
+// Fragment base addresses of a consumer warp. Fragment i of warp (wm, wn) covers rows
+// 8*(2i+wm) .. +7 and fragment j columns 8*(2j+wn) .. +7: interleaving spreads a ragged
+// tile's live fragments evenly over the four warps. For lane (fr = lane/4, fk = lane%4)
+// at k step ks (k = 4 ks + fk):
+//   A: 8 a_swz(k, 8(2i+wm) + fr) = ks*kAStepBytes + i*kFragStride + 8 (64 fk + ((8 wm + fr) ^ 4 fk))
+//      (the XOR touches bits 2-3 only, which 16 i leaves alone)
+//   B: kChunkBytes + 8 (k kBPitch + 8(2j+wn) + fr) = ks*kBStepBytes + j*kFragStride + b_base
 struct FragAddr {
-  std::uint32_t a[4][4], b[4][4];  // [k step][fragment]
+  std::uint32_t a, b;
 };
 
 __device__ __forceinline__ FragAddr frag_addresses(int wm, int wn, int fr, int fk) {
   FragAddr f;
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    const int k = ks * 4 + fk;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) f.a[ks][i] = 8u * a_swz(k, (2 * i + wm) * 8 + fr);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) f.b[ks][j] = kChunkBytes + (k * kBPitch + (2 * j + wn) * 8 + fr) * 8;
-  }
+  f.a = 8u * (fk * kBM + ((wm * 8 + fr) ^ (fk << 2)));
+  f.b = kChunkBytes + 8u * (fk * kBPitch + wn * 8 + fr);
   return f;
 }
 
 // Consumers: the K loop and epilogue of one GEMM tile (each element stored exactly once).
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
-                                                  std::uint32_t c0, const FragAddr& fa, std::uint32_t& it) {
+                                                  std::uint32_t cb, const FragAddr& fa, std::uint32_t& it) {
+  const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
   std::uint32_t nchunks = 0;
@@ -358,7 +387,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
   for (int i = 0; i < 4; ++i) {
     const int row = (2 * i + wm) * 8 + fr;
     if (row >= task.m) continue;
-    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + c0;  // row major, Q contiguous
+    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + cb * kCbPitch;  // point major
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = (2 * j + wn) * 8 + 2 * fk;
@@ -394,7 +423,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
         const std::uint32_t t = atomicAdd(tile_counter, 1u);
         post_item(c, seq, t);
         if (t >= ntiles) break;
-        produce_gemm_tile(p, c, p.tasks[t / col_blocks], (t % col_blocks) * kBN, &tm_wp, &tm_t, &tm_s, it,
+        produce_gemm_tile(p, c, p.tasks[t / col_blocks], t % col_blocks, &tm_wp, &tm_t, &tm_s, it,
                           [](const SegDev&) {});
       }
     }
@@ -405,7 +434,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   for (std::uint32_t seq = 0;; ++seq) {
     const std::uint64_t t = take_item(c, seq);
     if (t >= ntiles) break;
-    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks) * kBN, fa, it);
+    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks), fa, it);
   }
 }
 
@@ -480,7 +509,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
         const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
         const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-        produce_gemm_tile(p, c, task, cb * kBN, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
+        produce_gemm_tile(p, c, task, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
           if (sg.bbuf == kBufWp) return;  // Wp is complete: permute_in ran before this launch
           spin_until((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
                      d.node_tiles[sg.src] * kConsumerWarps);
@@ -499,7 +528,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
     const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-    consume_gemm_tile(p, c, task, cb * kBN, fa, it);
+    consume_gemm_tile(p, c, task, cb, fa, it);
     if (task.cbuf != kBufYp)  // leaf rows (Yp) have no dependent inside the launch
       warp_signal((task.cbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(task.node) * d.ncb + cb);
   }
@@ -515,7 +544,8 @@ __global__ void preset_done(const std::uint32_t* __restrict__ nodes, std::uint32
   done_t[static_cast<std::uint64_t>(node) * ncb + cb] = node_tiles[node] * kConsumerWarps;
 }
 
-// Transpose-permute into the point-major internal layout: Wp[ipmap[r], c] = W[r, c].
+// Transpose-permute into the point-major internal layout: Wp[ipmap[r], c] = W[r, c]
+// (column c at physical column phys_col(c)).
 // A 32 x 32 tile is read column by column (256 B contiguous per column of W), turned
 // around in shared memory and written row by row (256 B contiguous per point row of Wp),
 // so both sides move whole cache lines although the rows land in permuted order.
@@ -535,7 +565,7 @@ __global__ void __launch_bounds__(256) permute_in(const double* __restrict__ w, 
 #pragma unroll
   for (int k = 0; k < kTT; k += 8) {
     const std::uint32_t r = r0 + ty + k, c = c0 + tx;
-    if (r < n && c < q) wp[static_cast<std::uint64_t>(ipmap[r]) * ldwp + c] = tile[tx][ty + k];
+    if (r < n && c < q) wp[static_cast<std::uint64_t>(ipmap[r]) * ldwp + phys_col(c)] = tile[tx][ty + k];
   }
 }
 
@@ -549,7 +579,7 @@ __global__ void __launch_bounds__(256) permute_out(const double* __restrict__ yp
 #pragma unroll
   for (int k = 0; k < kTT; k += 8) {
     const std::uint32_t r = r0 + ty + k, c = c0 + tx;
-    tile[ty + k][tx] = (r < n && c < q) ? __ldg(yp + static_cast<std::uint64_t>(ipmap[r]) * ldyp + c) : 0.0;
+    tile[ty + k][tx] = (r < n && c < q) ? __ldg(yp + static_cast<std::uint64_t>(ipmap[r]) * ldyp + phys_col(c)) : 0.0;
   }
   __syncthreads();
 #pragma unroll

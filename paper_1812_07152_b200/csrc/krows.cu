@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(256) gen_ktiles(const double* __restrict__ pts
   }
 }
 
-// Y[r, c] = sum_s part[s*split_rows + r, c] (s ascending), point-major -> column major.
+// Y[r, c] = sum_s part[s*split_rows + r, c] (s ascending; column c at phys_col(c)),
+// point-major -> column major.
 __global__ void __launch_bounds__(256) reduce_splits(const double* __restrict__ part, std::uint64_t ldp,
                                                      std::uint32_t splits, std::uint64_t split_rows,
                                                      double* __restrict__ y, std::uint64_t ldy, std::uint32_t nrows,
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256) reduce_splits(const double* __restrict__ 
     const std::uint32_t r = r0 + ty + k, c = c0 + tx;
     double v = 0.0;
     if (r < nrows && c < q)
-      for (std::uint32_t s = 0; s < splits; ++s) v += part[(s * split_rows + r) * ldp + c];
+      for (std::uint32_t s = 0; s < splits; ++s) v += part[(s * split_rows + r) * ldp + phys_col(c)];
     tile[ty + k][tx] = v;
   }
   __syncthreads();
@@ -180,7 +181,10 @@ int ensure(T** p, std::size_t& cap, std::size_t count, bool zero = false) {
   *p = nullptr;
   cap = 0;
   HMXG_CUDA(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
-  if (zero) HMXG_CUDA(cudaMemset(*p, 0, count * sizeof(T)));
+  if (zero) {
+    HMXG_CUDA(cudaMemset(*p, 0, count * sizeof(T)));
+    HMXG_CUDA(cudaDeviceSynchronize());  // legacy-stream memset vs the non-blocking streams
+  }
   cap = count;
   return HMXG_OK;
 }
@@ -199,7 +203,7 @@ struct hmxg_points {
   std::uint32_t* ident = nullptr;  // identity order for the transpose kernel
   double* wdev = nullptr;          // host W staged on the device (n x q, column major)
   std::size_t wdev_cap = 0;
-  double* wt = nullptr;            // point-major W (npad x ldq); pad rows stay zero
+  double* wt = nullptr;            // point-major W (npad x phys_cols(q)); pad rows stay zero
   std::size_t wt_cap = 0;
   double* ktiles = nullptr;
   std::size_t ktiles_cap = 0;
@@ -245,7 +249,7 @@ int kernel_rows_dev(hmxg_points& P, const std::uint32_t* rows, std::uint64_t nro
   const std::uint64_t n = P.n, npad = P.npad;
   const std::uint32_t nkc = static_cast<std::uint32_t>(npad / kBK);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
-  const std::uint64_t ldq = (q + 7) / 8 * 8;
+  const std::uint64_t ldq = phys_cols(q);
   if (npad * ldq > P.wt_cap) {
     HMXG_CUDA(cudaStreamSynchronize(st));
     HMXG_TRY(ensure(&P.wt, P.wt_cap, npad * ldq, true));
@@ -263,7 +267,7 @@ int kernel_rows_dev(hmxg_points& P, const std::uint32_t* rows, std::uint64_t nro
     HMXG_CUDA(cudaMemcpyAsync(P.rows_dev, rows, nrows * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
   }
   CUtensorMap tm;
-  HMXG_TRY(make_map_box(&tm, P.wt, npad, q, ldq, kBPitch, kBK));
+  HMXG_TRY(make_map_box(&tm, P.wt, npad, ldq, ldq, kBPitch, kBK));
   const std::uint64_t rb_budget = std::max<std::uint64_t>(kBM, kTileBudgetBytes / (npad * 8) / kBM * kBM);
   const std::uint64_t rb = std::min<std::uint64_t>((nrows + kBM - 1) / kBM * kBM, rb_budget);
   const std::uint32_t ncb = (qq + kBN - 1) / kBN;

@@ -152,16 +152,20 @@ def split_evaluate(cds: CDS, w, parts: list["SplitPart"] | None = None, nparts: 
 
     if parts is None:
         parts = [SplitPart(cds, nparts, k, w.device.index or 0) for k in range(nparts)]
+    # every native call runs on torch's current stream, ordered with the tensor ops around it
+    from .executor import torch_stream
+
+    st = torch_stream(w.device)
     ys = [torch.zeros_like(w) for _ in parts]
     for part, y in zip(parts, ys):
-        part.stage(0, w.data_ptr(), y.data_ptr(), q)
+        part.stage(0, w.data_ptr(), y.data_ptr(), q, stream=st)
     count = parts[0].exchange_count()
     ts = [torch.empty(count, dtype=torch.float64, device=w.device) for _ in parts]
     for part, t in zip(parts, ts):
-        part.exchange(t.data_ptr(), count, to_matrix=False)
+        part.exchange(t.data_ptr(), count, to_matrix=False, stream=st)
     total = allreduce(torch.stack(ts).sum(0) if len(ts) > 1 else ts[0])
     for part in parts:
-        part.exchange(total.data_ptr(), count, to_matrix=True)
+        part.exchange(total.data_ptr(), count, to_matrix=True, stream=st)
     for part, y in zip(parts, ys):
-        part.stage(1, w.data_ptr(), y.data_ptr(), q)
+        part.stage(1, w.data_ptr(), y.data_ptr(), q, stream=st)
     return allreduce(torch.stack(ys).sum(0) if len(ys) > 1 else ys[0])

@@ -26,6 +26,19 @@ from . import _native as N
 from .cds import CDS
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def torch_stream(device=None) -> int:
+    """torch's current CUDA stream as a handle for the C-ABI. torch's default stream has the
+    handle 0, which the C-ABI reads as "the evaluator's internal stream", so it is passed as
+    cudaStreamLegacy instead (the calls are then ordered with torch's work)."""
+    import torch
+
+    h = torch.cuda.current_stream(device).cuda_stream
+    return h if h else CUDA_STREAM_LEGACY
+
+
 class HmxgError(RuntimeError):
     """A non-argument failure of the native evaluator (CUDA, memory, collective)."""
 

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_1812_07152_b200.executor import torch_stream
 from paper_1812_07152_b200 import CDS, EvalPlan, EvalStats, Evaluator, InstanceSpec, build_instance, config, evaluate
 
 pytestmark = pytest.mark.gpu
@@ -129,8 +130,7 @@ def test_device_pointer_path():
     ev = Evaluator(inst.cds)
     wd = torch.from_numpy(w.T.copy()).cuda()  # (q, n) row major == n x q column major
     yd = torch.empty_like(wd)
-    stream = torch.cuda.current_stream()
-    ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), 64, stream=stream.cuda_stream)
+    ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), 64, stream=torch_stream())
     torch.cuda.synchronize()
     y = yd.cpu().numpy().T
     assert np.array_equal(y, ev.evaluate(w))
@@ -146,11 +146,13 @@ def test_graph_replay_matches_direct_launches():
     s = torch.cuda.Stream()
     w = torch.randn((q, n), dtype=torch.float64, device="cuda")
     y_direct, y_graph = torch.empty_like(w), torch.empty_like(w)
+    s.wait_stream(torch.cuda.current_stream())  # W is written on torch's stream
     ev.evaluate_device(w.data_ptr(), y_direct.data_ptr(), q, stream=s.cuda_stream, sync=True, graph=False)
     for _ in range(2):  # capture, then replay
         ev.evaluate_device(w.data_ptr(), y_graph.data_ptr(), q, stream=s.cuda_stream, sync=True)
     assert torch.equal(y_direct, y_graph)
     w.copy_(torch.randn_like(w))  # same pointers, new data: the replay must read it
+    s.wait_stream(torch.cuda.current_stream())
     ev.evaluate_device(w.data_ptr(), y_graph.data_ptr(), q, stream=s.cuda_stream, sync=True)
     ev.evaluate_device(w.data_ptr(), y_direct.data_ptr(), q, stream=s.cuda_stream, sync=True, graph=False)
     assert torch.equal(y_direct, y_graph)

@@ -11,6 +11,7 @@ import pytest
 import oracle
 from paper_1812_07152_b200 import Evaluator, InstanceSpec, build_instance, config
 from paper_1812_07152_b200.distributed import SplitPart, split_evaluate
+from paper_1812_07152_b200.executor import torch_stream
 
 pytestmark = pytest.mark.gpu
 
@@ -27,7 +28,7 @@ def test_split_parts_equal_single_device(name, nparts, q):
     y = split_evaluate(inst.cds, w, parts=parts)
     ev = Evaluator(inst.cds)
     y_full = torch.empty_like(w)
-    ev.evaluate_device(w.data_ptr(), y_full.data_ptr(), q, sync=True)
+    ev.evaluate_device(w.data_ptr(), y_full.data_ptr(), q, sync=True, stream=torch_stream())
     assert torch.equal(y, y_full)
     yn = y.cpu().numpy().T
     assert oracle.rel_frob(yn, oracle.oracle_evaluate(inst.cds, w.cpu().numpy().T)) <= 1e-12
