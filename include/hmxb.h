@@ -30,7 +30,7 @@ enum hmxb_points_kind {
   HMXB_PTS_QUANTIZED = 4  /* U[0,1]^d quantized to `levels` values */
 };
 enum hmxb_kernel_kind {
-  HMXB_K_GAUSSIAN = 0,    /* exp(-|x-y|^2 / (2 h^2)) */
+  HMXB_K_GAUSSIAN = 0,    /* exp(-|x-y|^2 / (2 h h)), the reference's operation order */
   HMXB_K_EXPONENTIAL = 1, /* exp(-|x-y| / h) */
   HMXB_K_INVDIST = 2      /* 1/|x-y|, 1 on coincident points */
 };
@@ -57,6 +57,8 @@ typedef struct hmxb_spec {
   uint32_t knn_k;      /* neighbours per point for sampling / budget votes */
   uint32_t near_blocksize, far_blocksize, coarsen_p, coarsen_agg;
   uint32_t threads;    /* 0 -> hardware concurrency */
+  uint32_t skip_near;  /* 1: leave dgen empty (dptr still sized): the evaluator generates the
+                        * near blocks from the points (hmxg_upload_generated) */
 } hmxb_spec;
 
 typedef struct hmxb_build_stats {

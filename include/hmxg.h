@@ -171,6 +171,14 @@ int hmxg_split_exchange(hmxg_mat* mat, double* buf, size_t count, int to_matrix,
 int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y,
                   size_t ldy, unsigned flags, void* stream, hmxg_stats* stats);
 
+/* Upload with the near field generated on the device: cds.dgen is
+ * ignored (it may be NULL; dptr must still size every block) and every near block is
+ * evaluated from the points instead, D_ij(a, b) = K(x_{perm[start_i+a]}, x_{perm[start_j+b]})
+ * (compress.cpp:150-157), with the kernels of hmxg_points_upload. coords: n x d, point
+ * major, original point order (hmx::PointSet::coords). The host never forms or ships D. */
+int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
+                          double h, hmxg_mat** out);
+
 /* Launch sequence description; phase_get synchronizes the timing events of the last
  * HMXG_F_TIME_PHASES evaluation before filling last_ms. */
 int hmxg_phase_count(const hmxg_mat* mat);

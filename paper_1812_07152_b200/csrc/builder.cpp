@@ -102,8 +102,8 @@ double since(std::chrono::steady_clock::time_point t0) {
 struct KernelFn {
   int kind;
   double h;
-  double inv2h2, invh;
-  KernelFn(int k, double hh) : kind(k), h(hh), inv2h2(1.0 / (2.0 * hh * hh)), invh(1.0 / hh) {}
+  double den2h2, invh;  // 2 h h formed as (2 h) h, kernel.cpp:42
+  KernelFn(int k, double hh) : kind(k), h(hh), den2h2(2.0 * hh * hh), invh(1.0 / hh) {}
   double operator()(const double* x, const double* y, u32 d) const {
     double s = 0.0;
     for (u32 k = 0; k < d; ++k) {
@@ -112,7 +112,7 @@ struct KernelFn {
     }
     switch (kind) {
       case HMXB_K_GAUSSIAN:
-        return std::exp(-s * inv2h2);
+        return std::exp(-s / den2h2);
       case HMXB_K_EXPONENTIAL:
         return std::exp(-std::sqrt(s) * invh);
       default:
@@ -910,10 +910,10 @@ void pack(Instance& in) {
   for (u64 s = 0; s < nf; ++s)
     in.bptr[s + 1] = in.bptr[s] + u64(in.srank[in.far_flat[2 * s]]) * in.srank[in.far_flat[2 * s + 1]];
   for (u64 s = 0; s < nv; ++s) in.vptr[s + 1] = in.vptr[s] + in.basis[in.v_order[s]].size();
-  in.dgen.resize(in.dptr[nn]);
+  in.dgen.resize(in.spec.skip_near ? 0 : in.dptr[nn]);
   in.bgen.resize(in.bptr[nf]);
   in.vgen.resize(in.vptr[nv]);
-  parallel_for(nn, th, [&](u64 s) {
+  if (!in.spec.skip_near) parallel_for(nn, th, [&](u64 s) {
     const u32 i = in.near_flat[2 * s], j = in.near_flat[2 * s + 1];
     double* out = in.dgen.data() + in.dptr[s];
     const u32 mi = in.size(i);

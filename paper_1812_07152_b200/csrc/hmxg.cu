@@ -410,8 +410,43 @@ int compact_generators(const hmxg_cds_view& v, Plan& plan, const double* (&src)[
   return HMXG_OK;
 }
 
-int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split, hmxg_mat** out) {
+// The generated near field (hmxg_upload_generated): points and kernel of the CDS.
+struct NearSource {
+  const double* coords = nullptr;  // n x d, original point order
+  std::uint32_t d = 0;
+  KernelParams kp{};
+};
+
+// dgen on the device from the points: one NearBlock per near slot, in storage order.
+int generate_near(const hmxg_cds_view& v, const Plan& plan, const NearSource& src, double** gd, cudaStream_t st) {
+  *gd = nullptr;
+  if (plan.d_elems == 0) return HMXG_OK;
+  std::vector<NearBlock> blocks(v.num_near);
+  for (std::uint64_t s = 0; s < v.num_near; ++s) {
+    const std::uint32_t i = v.near_pairs[2 * s], j = v.near_pairs[2 * s + 1];
+    blocks[s] = NearBlock{v.dptr[s], v.start[i], v.end[i] - v.start[i], v.start[j], v.end[j] - v.start[j]};
+  }
+  double* pts = nullptr;
+  std::uint32_t* perm = nullptr;
+  NearBlock* dblocks = nullptr;
+  HMXG_TRY(dev_upload(&pts, src.coords, v.n * src.d, st));
+  HMXG_TRY(dev_upload(&perm, v.perm, v.n, st));
+  HMXG_TRY(dev_upload(&dblocks, blocks.data(), blocks.size(), st));
+  HMXG_CUDA(cudaMalloc(gd, plan.d_elems * sizeof(double)));
+  gen_near<<<static_cast<unsigned>(std::min<std::uint64_t>(blocks.size(), 148ull * 16)), 256, 0, st>>>(
+      pts, src.kp, perm, dblocks, blocks.size(), *gd);
+  HMXG_CUDA(cudaGetLastError());
+  HMXG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(pts);
+  cudaFree(perm);
+  cudaFree(dblocks);
+  return HMXG_OK;
+}
+
+int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split, hmxg_mat** out,
+                const NearSource* near_src = nullptr) {
   if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
+  if (near_src && split.nparts > 1) return set_err(HMXG_EINVAL, "hmxg_upload: generated near field is single-part");
   *out = nullptr;
   auto mat = std::make_unique<hmxg_mat>();
   mat->ctx = ctx;
@@ -453,7 +488,10 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     double *gd = nullptr, *gb = nullptr, *gv = nullptr;
     TileSrc* srcs = nullptr;
     std::uint32_t* cseg = nullptr;
-    HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
+    if (near_src)
+      HMXG_TRY(generate_near(*cds, plan, *near_src, &gd, d.comp));
+    else
+      HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
     HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
     HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
     HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
@@ -544,6 +582,24 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
 
 int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
   return upload_impl(ctx, cds, SplitSpec{}, out);
+}
+
+int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
+                          double h, hmxg_mat** out) {
+  if (!cds || !coords || d == 0) return set_err(HMXG_EINVAL, "hmxg_upload_generated: null points");
+  if (kernel < HMXG_KERNEL_GAUSSIAN || kernel > HMXG_KERNEL_INVDIST)
+    return set_err(HMXG_EINVAL, "hmxg_upload_generated: unknown kernel");
+  if (kernel != HMXG_KERNEL_INVDIST && !(h > 0.0)) return set_err(HMXG_EINVAL, "Gaussian kernel: bandwidth must be > 0");
+  NearSource src;
+  src.coords = coords;
+  src.d = d;
+  src.kp.kind = kernel;
+  src.kp.d = d;
+  src.kp.den = 2.0 * h * h;
+  src.kp.invh = 1.0 / h;
+  SplitSpec spec;
+  spec.generated_near = true;
+  return upload_impl(ctx, cds, spec, out, &src);
 }
 
 int hmxg_upload_split(hmxg_ctx* ctx, const hmxg_cds_view* cds, uint32_t nparts, uint32_t part, hmxg_mat** out) {

@@ -136,6 +136,52 @@ __device__ __forceinline__ std::uint64_t pick_ld(const GemmParams& p, unsigned b
 // half-warp is one wavefront (rows are 512 B apart and would otherwise collide).
 __host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 2)); }
 
+// ---------------------------------------------------------------- kernel functions
+// K(x, y) on the device, for the generated near field and the error oracle (krows.cu).
+struct KernelParams {
+  int kind;
+  std::uint32_t d;
+  double den;   // gaussian: 2 h h, formed as (2.0 * h) * h like kernel.cpp:42
+  double invh;  // exponential: 1 / h
+};
+
+// K(x, y) with the reference's operation order: the squared distance accumulates the
+// rounded products dimension by dimension (no FMA contraction, kernel.cpp:37-41).
+__device__ __forceinline__ double kernel_value(const KernelParams& kp, const double* __restrict__ x,
+                                               const double* __restrict__ y) {
+  double s = 0.0;
+  for (std::uint32_t i = 0; i < kp.d; ++i) {
+    const double t = __dsub_rn(__ldg(x + i), __ldg(y + i));
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  if (kp.kind == HMXG_KERNEL_GAUSSIAN) return exp(__ddiv_rn(-s, kp.den));
+  if (kp.kind == HMXG_KERNEL_EXPONENTIAL) return exp(__dmul_rn(-__dsqrt_rn(s), kp.invh));
+  return s == 0.0 ? 1.0 : __ddiv_rn(1.0, __dsqrt_rn(s));
+}
+
+// One near block of the generated near field: D_ij = K(x_{perm[start_i + a]},
+// x_{perm[start_j + b]}), m_i x m_j column major at element offset off of dgen
+// (compress.cpp:150-157 / dense_block, kernel.cpp:52-65, in the CDS's storage order).
+struct NearBlock {
+  std::uint64_t off;
+  std::uint32_t start_i, m_i, start_j, m_j;
+};
+
+__global__ void __launch_bounds__(256) gen_near(const double* __restrict__ pts, const KernelParams kp,
+                                                const std::uint32_t* __restrict__ perm,
+                                                const NearBlock* __restrict__ blocks, std::uint64_t nblocks,
+                                                double* __restrict__ dgen) {
+  for (std::uint64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
+    const NearBlock b = blocks[s];
+    const std::uint32_t count = b.m_i * b.m_j;
+    for (std::uint32_t e = threadIdx.x; e < count; e += blockDim.x) {
+      const std::uint32_t a = e % b.m_i, c = e / b.m_i;  // consecutive threads: consecutive rows
+      const std::uint64_t pi = perm[b.start_i + a], pj = perm[b.start_j + c];
+      dgen[b.off + e] = kernel_value(kp, pts + pi * kp.d, pts + pj * kp.d);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- A pre-tiling
 __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
                        const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,

@@ -33,27 +33,6 @@
 namespace hmxg {
 namespace {
 
-struct KernelParams {
-  int kind;
-  std::uint32_t d;
-  double den;   // gaussian: 2 h h, formed as (2.0 * h) * h like kernel.cpp:42
-  double invh;  // exponential: 1 / h
-};
-
-// K(x, y) with the reference's operation order: the squared distance accumulates the
-// rounded products dimension by dimension (no FMA contraction, kernel.cpp:37-41).
-__device__ __forceinline__ double kernel_value(const KernelParams& kp, const double* __restrict__ x,
-                                               const double* __restrict__ y) {
-  double s = 0.0;
-  for (std::uint32_t i = 0; i < kp.d; ++i) {
-    const double t = __dsub_rn(__ldg(x + i), __ldg(y + i));
-    s = __dadd_rn(s, __dmul_rn(t, t));
-  }
-  if (kp.kind == HMXG_KERNEL_GAUSSIAN) return exp(__ddiv_rn(-s, kp.den));
-  if (kp.kind == HMXG_KERNEL_EXPONENTIAL) return exp(__dmul_rn(-__dsqrt_rn(s), kp.invh));
-  return s == 0.0 ? 1.0 : __ddiv_rn(1.0, __dsqrt_rn(s));
-}
-
 // A chunks of K(x_rows, x_all) for one block of output rows: chunk c = (row tile t, K
 // chunk kc) holds A(r, k) = K(x_{row(t*64+r)}, x_{kc*16+k}) at a_swz(k, r), zero outside.
 __global__ void __launch_bounds__(256) gen_ktiles(const double* __restrict__ pts, const KernelParams kp,

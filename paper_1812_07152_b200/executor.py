@@ -148,13 +148,23 @@ class Context:
 class Evaluator:
     """A CDS resident on the devices of a context (``hmxg_upload``)."""
 
-    def __init__(self, cds: CDS, devices=(0,), context: Context | None = None):
+    def __init__(self, cds: CDS, devices=(0,), context: Context | None = None, points: np.ndarray | None = None,
+                 kernel=None):
+        """``points``/``kernel`` (an accuracy.Kernel): generate the near field on the device
+        from the points (hmxg_upload_generated); the CDS's dgen is then not read."""
         self.cds = cds
         self.ctx = context or Context(devices)
         self._own_ctx = context is None
         h = C.c_void_p()
         v = cds.view()
-        _check(N.hmxg().hmxg_upload(self.ctx.handle, C.byref(v), C.byref(h)))
+        if points is None:
+            _check(N.hmxg().hmxg_upload(self.ctx.handle, C.byref(v), C.byref(h)))
+        else:
+            pts = np.ascontiguousarray(points, dtype=np.float64)
+            if pts.ndim != 2 or pts.shape[0] != cds.n:
+                raise ValueError("Evaluator: points must be an n x d array")
+            _check(N.hmxg().hmxg_upload_generated(self.ctx.handle, C.byref(v), pts.ctypes.data_as(C.c_void_p),
+                                                  pts.shape[1], kernel.code, kernel.h, C.byref(h)))
         self._h = h
         self._lock = threading.Lock()
 

@@ -46,6 +46,7 @@ class InstanceSpec:
     coarsen_p: int = 8
     coarsen_agg: int = 2
     threads: int = 0
+    skip_near: bool = False  # leave dgen empty: Evaluator.generated() builds D on the device
 
     def to_native(self) -> N.BuildSpec:
         s = N.BuildSpec()
