@@ -228,6 +228,23 @@ uint64_t hmxg_sample_rows(uint64_t n, uint64_t seed, uint32_t* rows);
 int hmxg_relative_error(hmxg_points* pts, const double* Y_approx, size_t ldya, const double* W, size_t n, size_t q,
                         size_t ldw, int mode, uint64_t seed, unsigned flags, double* eps);
 
+/* ---- GPU compression: the interpolative decomposition of every
+ * participating node, bottom-up (compress.cpp:17-148). Inputs: the points (n x d, original
+ * order) and kernel, the tree (lchild/rchild/start/end/level/perm, num_nodes entries, perm n),
+ * participation flags, and the sample rows per node in CSR form (sample_ptr[num_nodes + 1]
+ * offsets into sample_idx, point indices; hmx::SampleInfo::rows). Per node the result is
+ * its srank, its skeleton (point indices) and V (rows = the node's column count, srank
+ * columns, column major), read with hmxg_compressed_get (CSR over nodes). */
+typedef struct hmxg_compressed hmxg_compressed;
+int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, int32_t kernel, double h,
+                  uint32_t num_nodes, const uint32_t* lchild, const uint32_t* rchild, const uint32_t* start,
+                  const uint32_t* end, const uint32_t* level, const uint32_t* perm, const uint8_t* participating,
+                  const uint64_t* sample_ptr, const uint32_t* sample_idx, double bacc, uint32_t max_rank,
+                  hmxg_compressed** out);
+int hmxg_compressed_get(const hmxg_compressed* c, const uint32_t** srank, const uint64_t** skel_ptr,
+                        const uint32_t** skel, const uint64_t** v_ptr, const uint64_t** v_rows, const double** v);
+void hmxg_compressed_free(hmxg_compressed* c);
+
 const char* hmxg_last_error(void);
 const char* hmxg_version(void);
 

@@ -72,6 +72,9 @@ def _ref_lib():
             "hmxr_relative_error_vs": (C.c_int, [vp, vp, vp, u64, u64, C.c_int32, u64, C.POINTER(C.c_double)]),
             "hmxr_dense_apply_points": (C.c_int, [vp, u64, u64, C.c_int32, C.c_double, vp, u64, vp]),
             "hmxr_sample_rows": (u64, [u64, u64, vp]),
+            "hmxr_samples": (C.c_int, [vp, vp, vp]),
+            "hmxr_basis": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(u64), vp, vp]),
+            "hmxr_compress_seconds": (C.c_double, [vp]),
             "hmxr_mix64": (u64, [u64]),
             "hmxr_rng_fill_pm1": (None, [u64, u64, vp]),
             "hmxr_last_error": (C.c_char_p, []),
@@ -203,6 +206,25 @@ class RefInstance:
                                                      wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1], mode,
                                                      seed, C.byref(eps)))
         return eps.value
+
+    def samples(self) -> tuple[np.ndarray, np.ndarray]:
+        """SampleInfo rows per node as CSR (sample_ptr[num_nodes + 1], sample_idx)."""
+        nn = self.cds.num_nodes
+        ptr = np.zeros(nn + 1, dtype=np.uint64)
+        _ref_lib().hmxr_samples(self._h, ptr.ctypes.data_as(C.c_void_p), None)
+        idx = np.zeros(int(ptr[-1]), dtype=np.uint32)
+        _ref_lib().hmxr_samples(self._h, None, idx.ctypes.data_as(C.c_void_p))
+        return ptr, idx
+
+    def basis(self, node: int) -> tuple[int, np.ndarray, np.ndarray]:
+        """(srank, skeleton point indices, V as rows x srank) of the reference's compress."""
+        sr, rows = C.c_uint32(), C.c_uint64()
+        _ref_check(_ref_lib().hmxr_basis(self._h, node, C.byref(sr), C.byref(rows), None, None))
+        skel = np.zeros(sr.value, dtype=np.uint32)
+        v = np.zeros((rows.value, sr.value), dtype=np.float64, order="F")
+        _ref_check(_ref_lib().hmxr_basis(self._h, node, C.byref(sr), C.byref(rows), skel.ctypes.data_as(C.c_void_p),
+                                         v.ctypes.data_as(C.c_void_p)))
+        return sr.value, skel, v
 
     def points(self) -> np.ndarray:
         p, n, d = C.POINTER(C.c_double)(), C.c_uint64(), C.c_uint64()

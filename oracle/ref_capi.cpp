@@ -76,6 +76,7 @@ struct RefInstance {
   // flattened pair lists for the view
   std::vector<std::uint32_t> near_flat, far_flat;
   std::vector<std::uint8_t> part;
+  double compress_seconds = 0.0;
 };
 
 void flatten(const hmx::CDS& cds, std::vector<std::uint32_t>& nf, std::vector<std::uint32_t>& ff) {
@@ -204,7 +205,9 @@ int hmxr_instance_new(const hmxr_spec* s, void** out) {
     in->si = hmx::build_samples(in->pts, in->ht.tree, knn, s->budget,
                                 s->sample_exact ? hmx::SampleMode::Exact : hmx::SampleMode::Neighbor,
                                 s->seed);
+    const auto tc = std::chrono::steady_clock::now();
     in->cm = hmx::compress(in->ht, in->kernel, in->pts, in->si, s->bacc, s->max_rank);
+    in->compress_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - tc).count();
     in->nbs = hmx::blocking(in->ht, s->near_bs, hmx::BlockKind::Near);
     in->fbs = hmx::blocking(in->ht, s->far_bs, hmx::BlockKind::Far);
     in->cs = hmx::coarsening(in->ht.tree, hmx::srank_vector(in->cm), in->cm.participating, s->p, s->agg);
@@ -417,6 +420,34 @@ std::uint64_t hmxr_sample_rows(std::uint64_t n, std::uint64_t seed, std::uint32_
   std::copy(all.begin(), all.begin() + nr, rows);
   return nr;
 }
+
+// The compression inputs and outputs of a reference instance (compress.cpp:102-148):
+// sample rows per node as CSR, and each node's basis (srank, skeleton, V rows x srank).
+int hmxr_samples(void* inst, std::uint64_t* ptr, std::uint32_t* idx) {
+  auto* in = static_cast<RefInstance*>(inst);
+  std::uint64_t off = 0;
+  for (std::size_t node = 0; node < in->si.rows.size(); ++node) {
+    if (ptr) ptr[node] = off;
+    if (idx) std::copy(in->si.rows[node].begin(), in->si.rows[node].end(), idx + off);
+    off += in->si.rows[node].size();
+  }
+  if (ptr) ptr[in->si.rows.size()] = off;
+  return 0;
+}
+
+int hmxr_basis(void* inst, std::uint32_t node, std::uint32_t* srank, std::uint64_t* rows, std::uint32_t* skel,
+               double* v) {
+  auto* in = static_cast<RefInstance*>(inst);
+  if (node >= in->cm.bases.size()) return 1;
+  const auto& b = in->cm.bases[node];
+  *srank = b.srank;
+  *rows = b.v.rows;
+  if (skel) std::copy(b.skeleton.begin(), b.skeleton.end(), skel);
+  if (v && b.v.data.size()) std::memcpy(v, b.v.data.data(), b.v.data.size() * sizeof(double));
+  return 0;
+}
+
+double hmxr_compress_seconds(void* inst) { return static_cast<RefInstance*>(inst)->compress_seconds; }
 
 // The reference RNG primitives, so the CLI's random W (hmx.cpp:117-122) can be pinned.
 std::uint64_t hmxr_mix64(std::uint64_t x) { return hmx::mix64(x); }

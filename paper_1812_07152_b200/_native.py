@@ -195,6 +195,13 @@ HMXG_SYMBOLS = {
     "hmxg_sample_rows": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_void_p]),
     "hmxg_relative_error": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_size_t,
                                       C.c_size_t, C.c_int, C.c_uint64, C.c_uint, C.POINTER(C.c_double)]),
+    "hmxg_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_double, C.c_uint32,
+                                _u32p, _u32p, _u32p, _u32p, _u32p, _u32p, C.POINTER(C.c_uint8),
+                                C.POINTER(C.c_uint64), _u32p, C.c_double, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "hmxg_compressed_get": (C.c_int, [C.c_void_p, C.POINTER(_u32p), C.POINTER(C.POINTER(C.c_uint64)),
+                                      C.POINTER(_u32p), C.POINTER(C.POINTER(C.c_uint64)),
+                                      C.POINTER(C.POINTER(C.c_uint64)), C.POINTER(_f64p)]),
+    "hmxg_compressed_free": (None, [C.c_void_p]),
     "hmxg_last_error": (C.c_char_p, []),
     "hmxg_version": (C.c_char_p, []),
 }

@@ -19,6 +19,7 @@
 
 #include <cstdint>
 
+#include "kfun.cuh"
 #include "plan.hpp"
 
 namespace hmxg {
@@ -135,29 +136,6 @@ __device__ __forceinline__ std::uint64_t pick_ld(const GemmParams& p, unsigned b
 // XOR on bits 2-3 of r moves the four k rows to four disjoint 8-bank groups, so each
 // half-warp is one wavefront (rows are 512 B apart and would otherwise collide).
 __host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 2)); }
-
-// ---------------------------------------------------------------- kernel functions
-// K(x, y) on the device, for the generated near field and the error oracle (krows.cu).
-struct KernelParams {
-  int kind;
-  std::uint32_t d;
-  double den;   // gaussian: 2 h h, formed as (2.0 * h) * h like kernel.cpp:42
-  double invh;  // exponential: 1 / h
-};
-
-// K(x, y) with the reference's operation order: the squared distance accumulates the
-// rounded products dimension by dimension (no FMA contraction, kernel.cpp:37-41).
-__device__ __forceinline__ double kernel_value(const KernelParams& kp, const double* __restrict__ x,
-                                               const double* __restrict__ y) {
-  double s = 0.0;
-  for (std::uint32_t i = 0; i < kp.d; ++i) {
-    const double t = __dsub_rn(__ldg(x + i), __ldg(y + i));
-    s = __dadd_rn(s, __dmul_rn(t, t));
-  }
-  if (kp.kind == HMXG_KERNEL_GAUSSIAN) return exp(__ddiv_rn(-s, kp.den));
-  if (kp.kind == HMXG_KERNEL_EXPONENTIAL) return exp(__dmul_rn(-__dsqrt_rn(s), kp.invh));
-  return s == 0.0 ? 1.0 : __ddiv_rn(1.0, __dsqrt_rn(s));
-}
 
 // One near block of the generated near field: D_ij = K(x_{perm[start_i + a]},
 // x_{perm[start_j + b]}), m_i x m_j column major at element offset off of dgen
