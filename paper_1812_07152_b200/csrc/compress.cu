@@ -282,10 +282,27 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
   for (std::uint32_t i = 0; i < num_nodes; ++i)
     if (participating[i]) by_level[level[i]].push_back(i);
 
-  IdJob* d_jobs = nullptr;
-  std::uint32_t* d_cols = nullptr;
-  double *d_scratch = nullptr, *d_vout = nullptr;
-  std::uint32_t *d_piv = nullptr, *d_rank = nullptr;
+  // per-level buffers, grown as needed and freed on every exit path
+  struct LevelBufs {
+    IdJob* jobs = nullptr;
+    std::uint32_t* cols = nullptr;
+    double *scratch = nullptr, *vout = nullptr;
+    std::uint32_t *piv = nullptr, *rank = nullptr;
+    ~LevelBufs() {
+      cudaFree(jobs);
+      cudaFree(cols);
+      cudaFree(scratch);
+      cudaFree(vout);
+      cudaFree(piv);
+      cudaFree(rank);
+    }
+  } lb;
+  IdJob*& d_jobs = lb.jobs;
+  std::uint32_t*& d_cols = lb.cols;
+  double*& d_scratch = lb.scratch;
+  double*& d_vout = lb.vout;
+  std::uint32_t*& d_piv = lb.piv;
+  std::uint32_t*& d_rank = lb.rank;
   std::size_t cap_jobs = 0, cap_cols = 0, cap_scratch = 0, cap_vout = 0, cap_piv = 0, cap_rank = 0;
   for (std::uint32_t lvl = height + 1; lvl-- > 0;) {  // deepest level first (compress.cpp:117-121)
     std::vector<IdJob> jobs;
@@ -359,9 +376,6 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
       vmat[node].assign(vh.begin() + jobs[q].out_off, vh.begin() + jobs[q].out_off + std::uint64_t(c) * k);
     }
   }
-  for (void* p : {static_cast<void*>(d_jobs), static_cast<void*>(d_cols), static_cast<void*>(d_scratch),
-                  static_cast<void*>(d_vout), static_cast<void*>(d_piv), static_cast<void*>(d_rank)})
-    guard.ptrs.push_back(p);
   // flatten
   res->skel_ptr.assign(num_nodes + 1, 0);
   res->v_ptr.assign(num_nodes + 1, 0);
