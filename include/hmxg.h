@@ -171,13 +171,16 @@ int hmxg_split_exchange(hmxg_mat* mat, double* buf, size_t count, int to_matrix,
 int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw, double* Y,
                   size_t ldy, unsigned flags, void* stream, hmxg_stats* stats);
 
-/* Upload with the near field generated on the device: cds.dgen is
+/* Upload with the kernel blocks generated on the device: cds.dgen is
  * ignored (it may be NULL; dptr must still size every block) and every near block is
  * evaluated from the points instead, D_ij(a, b) = K(x_{perm[start_i+a]}, x_{perm[start_j+b]})
- * (compress.cpp:150-157), with the kernels of hmxg_points_upload. coords: n x d, point
- * major, original point order (hmx::PointSet::coords). The host never forms or ships D. */
+ * (compress.cpp:143-147), with the kernels of hmxg_points_upload. coords: n x d, point
+ * major, original point order (hmx::PointSet::coords). The host never forms or ships D.
+ * With skel_ptr (num_nodes + 1 CSR offsets into skel_idx: every node's skeleton point
+ * indices, srank of them, e.g. from hmxg_compress) the far blocks are generated as well,
+ * B_ij = K(skeleton_i, skeleton_j) (compress.cpp:139-142), and cds.bgen is ignored. */
 int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
-                          double h, hmxg_mat** out);
+                          double h, const uint64_t* skel_ptr, const uint32_t* skel_idx, hmxg_mat** out);
 
 /* Launch sequence description; phase_get synchronizes the timing events of the last
  * HMXG_F_TIME_PHASES evaluation before filling last_ms. */

@@ -173,7 +173,7 @@ HMXG_SYMBOLS = {
          C.c_uint, C.c_void_p, C.POINTER(Stats)],
     ),
     "hmxg_upload_generated": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_void_p, C.c_uint32, C.c_int32,
-                                        C.c_double, C.POINTER(C.c_void_p)]),
+                                        C.c_double, C.POINTER(C.c_uint64), _u32p, C.POINTER(C.c_void_p)]),
     "hmxg_upload_split": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "hmxg_split_stage": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p,
                                    C.c_size_t, C.c_void_p]),

@@ -73,3 +73,34 @@ def gpu_compress(points: np.ndarray, kernel: Kernel, cds: CDS, sample_ptr: np.nd
         if h:
             lib.hmxg_compressed_free(h)
         ctx.close()
+
+
+def skeleton_csr(bases: list[NodeBasis]) -> tuple[np.ndarray, np.ndarray]:
+    """(skel_ptr, skel_idx) over nodes, for Evaluator(skeletons=...)."""
+    ptr = np.zeros(len(bases) + 1, dtype=np.uint64)
+    for i, b in enumerate(bases):
+        ptr[i + 1] = ptr[i] + b.skeleton.size
+    idx = np.concatenate([b.skeleton for b in bases]).astype(np.uint32) if ptr[-1] else np.zeros(0, np.uint32)
+    return ptr, idx
+
+
+def cds_from_bases(structure: CDS, bases: list[NodeBasis]) -> CDS:
+    """A CDS with ``structure``'s tree, pair lists and storage orders and the V generators
+    of ``bases`` (vgen in v_order, each V column major: structure.hpp:104-128); dgen and
+    bgen are left empty for the device to generate (Evaluator(points=, skeletons=))."""
+    for i, b in enumerate(bases):
+        if b.srank != int(structure.sranks[i]):
+            raise ValueError(f"cds_from_bases: node {i} has srank {b.srank}, the structure {int(structure.sranks[i])}")
+    vptr = np.zeros(structure.v_order.size + 1, dtype=np.uint64)
+    parts = []
+    for s, node in enumerate(structure.v_order):
+        v = bases[int(node)].v
+        parts.append(np.asfortranarray(v).ravel(order="F"))
+        vptr[s + 1] = vptr[s] + v.size
+    if not np.array_equal(vptr, structure.vptr):
+        raise ValueError("cds_from_bases: V sizes differ from the structure's vptr")
+    kw = {k: getattr(structure, k) for k in structure.__dataclass_fields__ if k not in ("owner", "_cache")}
+    kw["vgen"] = np.concatenate(parts) if parts else np.zeros(0)
+    kw["dgen"] = np.zeros(0)
+    kw["bgen"] = np.zeros(0)
+    return CDS(**kw)

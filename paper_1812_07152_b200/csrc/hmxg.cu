@@ -410,37 +410,58 @@ int compact_generators(const hmxg_cds_view& v, Plan& plan, const double* (&src)[
   return HMXG_OK;
 }
 
-// The generated near field (hmxg_upload_generated): points and kernel of the CDS.
+// Generated blocks (hmxg_upload_generated): the points and kernel of the CDS, and
+// optionally every node's skeleton (CSR) to generate the far blocks too.
 struct NearSource {
   const double* coords = nullptr;  // n x d, original point order
   std::uint32_t d = 0;
   KernelParams kp{};
+  const std::uint64_t* skel_ptr = nullptr;  // num_nodes + 1, or null: bgen comes from the view
+  const std::uint32_t* skel_idx = nullptr;
 };
 
-// dgen on the device from the points: one NearBlock per near slot, in storage order.
-int generate_near(const hmxg_cds_view& v, const Plan& plan, const NearSource& src, double** gd, cudaStream_t st) {
-  *gd = nullptr;
-  if (plan.d_elems == 0) return HMXG_OK;
-  std::vector<NearBlock> blocks(v.num_near);
-  for (std::uint64_t s = 0; s < v.num_near; ++s) {
-    const std::uint32_t i = v.near_pairs[2 * s], j = v.near_pairs[2 * s + 1];
-    blocks[s] = NearBlock{v.dptr[s], v.start[i], v.end[i] - v.start[i], v.start[j], v.end[j] - v.start[j]};
-  }
-  double* pts = nullptr;
-  std::uint32_t* perm = nullptr;
-  NearBlock* dblocks = nullptr;
-  HMXG_TRY(dev_upload(&pts, src.coords, v.n * src.d, st));
-  HMXG_TRY(dev_upload(&perm, v.perm, v.n, st));
+// Kernel blocks on the device, one GenBlock per slot in storage order, into *out.
+int generate_blocks(const double* pts, const KernelParams& kp, const std::vector<std::uint32_t>& idx,
+                    const std::vector<GenBlock>& blocks, std::uint64_t elems, double** out, cudaStream_t st) {
+  *out = nullptr;
+  if (elems == 0) return HMXG_OK;
+  std::uint32_t* didx = nullptr;
+  GenBlock* dblocks = nullptr;
+  HMXG_TRY(dev_upload(&didx, idx.data(), idx.size(), st));
   HMXG_TRY(dev_upload(&dblocks, blocks.data(), blocks.size(), st));
-  HMXG_CUDA(cudaMalloc(gd, plan.d_elems * sizeof(double)));
-  gen_near<<<static_cast<unsigned>(std::min<std::uint64_t>(blocks.size(), 148ull * 16)), 256, 0, st>>>(
-      pts, src.kp, perm, dblocks, blocks.size(), *gd);
+  HMXG_CUDA(cudaMalloc(out, elems * sizeof(double)));
+  gen_blocks<<<static_cast<unsigned>(std::min<std::uint64_t>(blocks.size(), 148ull * 16)), 256, 0, st>>>(
+      pts, kp, didx, dblocks, blocks.size(), *out);
   HMXG_CUDA(cudaGetLastError());
   HMXG_CUDA(cudaStreamSynchronize(st));
-  cudaFree(pts);
-  cudaFree(perm);
+  cudaFree(didx);
   cudaFree(dblocks);
   return HMXG_OK;
+}
+
+// dgen (and, with skeletons, bgen) on the device from the points.
+int generate_generators(const hmxg_cds_view& v, const Plan& plan, const NearSource& src, double** gd, double** gb,
+                        cudaStream_t st) {
+  double* pts = nullptr;
+  HMXG_TRY(dev_upload(&pts, src.coords, v.n * src.d, st));
+  std::vector<GenBlock> blocks(v.num_near);
+  for (std::uint64_t s = 0; s < v.num_near; ++s) {
+    const std::uint32_t i = v.near_pairs[2 * s], j = v.near_pairs[2 * s + 1];
+    blocks[s] = GenBlock{v.dptr[s], v.start[i], v.start[j], v.end[i] - v.start[i], v.end[j] - v.start[j]};
+  }
+  const std::vector<std::uint32_t> perm(v.perm, v.perm + v.n);
+  int rc = generate_blocks(pts, src.kp, perm, blocks, plan.d_elems, gd, st);
+  if (rc == HMXG_OK && src.skel_ptr) {
+    blocks.assign(v.num_far, GenBlock{});
+    for (std::uint64_t s = 0; s < v.num_far; ++s) {
+      const std::uint32_t i = v.far_pairs[2 * s], j = v.far_pairs[2 * s + 1];
+      blocks[s] = GenBlock{v.bptr[s], src.skel_ptr[i], src.skel_ptr[j], v.sranks[i], v.sranks[j]};
+    }
+    const std::vector<std::uint32_t> skel(src.skel_idx, src.skel_idx + src.skel_ptr[v.num_nodes]);
+    rc = generate_blocks(pts, src.kp, skel, blocks, plan.b_elems, gb, st);
+  }
+  cudaFree(pts);
+  return rc;
 }
 
 int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split, hmxg_mat** out,
@@ -489,10 +510,10 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     TileSrc* srcs = nullptr;
     std::uint32_t* cseg = nullptr;
     if (near_src)
-      HMXG_TRY(generate_near(*cds, plan, *near_src, &gd, d.comp));
+      HMXG_TRY(generate_generators(*cds, plan, *near_src, &gd, &gb, d.comp));
     else
       HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
-    HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
+    if (!near_src || !near_src->skel_ptr) HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
     HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
     HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
     HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
@@ -585,8 +606,17 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
 }
 
 int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
-                          double h, hmxg_mat** out) {
+                          double h, const uint64_t* skel_ptr, const uint32_t* skel_idx, hmxg_mat** out) {
   if (!cds || !coords || d == 0) return set_err(HMXG_EINVAL, "hmxg_upload_generated: null points");
+  if (skel_ptr) {  // every node's skeleton must have its srank entries, all of them points
+    if (cds->num_nodes && !cds->sranks) return set_err(HMXG_EINVAL, "cds: null array in view");
+    if (skel_ptr[cds->num_nodes] && !skel_idx) return set_err(HMXG_EINVAL, "hmxg_upload_generated: null skeletons");
+    for (std::uint32_t i = 0; i < cds->num_nodes; ++i)
+      if (skel_ptr[i + 1] - skel_ptr[i] != cds->sranks[i])
+        return set_err(HMXG_EINVAL, "hmxg_upload_generated: skeleton size differs from the node's srank");
+    for (std::uint64_t s = 0; s < skel_ptr[cds->num_nodes]; ++s)
+      if (skel_idx[s] >= cds->n) return set_err(HMXG_EINVAL, "dense_block: row index out of range");
+  }
   if (kernel < HMXG_KERNEL_GAUSSIAN || kernel > HMXG_KERNEL_INVDIST)
     return set_err(HMXG_EINVAL, "hmxg_upload_generated: unknown kernel");
   if (kernel != HMXG_KERNEL_INVDIST && !(h > 0.0)) return set_err(HMXG_EINVAL, "Gaussian kernel: bandwidth must be > 0");
@@ -597,8 +627,11 @@ int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double*
   src.kp.d = d;
   src.kp.den = 2.0 * h * h;
   src.kp.invh = 1.0 / h;
+  src.skel_ptr = skel_ptr;
+  src.skel_idx = skel_idx;
   SplitSpec spec;
   spec.generated_near = true;
+  spec.generated_far = skel_ptr != nullptr;
   return upload_impl(ctx, cds, spec, out, &src);
 }
 

@@ -137,25 +137,27 @@ __device__ __forceinline__ std::uint64_t pick_ld(const GemmParams& p, unsigned b
 // half-warp is one wavefront (rows are 512 B apart and would otherwise collide).
 __host__ __device__ __forceinline__ int a_swz(int k, int r) { return k * kBM + (r ^ ((k & 3) << 2)); }
 
-// One near block of the generated near field: D_ij = K(x_{perm[start_i + a]},
-// x_{perm[start_j + b]}), m_i x m_j column major at element offset off of dgen
-// (compress.cpp:150-157 / dense_block, kernel.cpp:52-65, in the CDS's storage order).
-struct NearBlock {
+// One generated kernel block: G(a, b) = K(x_{idx[rows + a]}, x_{idx[cols + b]}), m x ncols
+// column major at element offset off. Near blocks index the tree permutation
+// (idx = perm, rows = start_i: the node's points, compress.cpp:143-147); far blocks index
+// the concatenated skeletons (compress.cpp:139-142). dense_block, kernel.cpp:52-65.
+struct GenBlock {
   std::uint64_t off;
-  std::uint32_t start_i, m_i, start_j, m_j;
+  std::uint64_t rows, cols;  // offsets into idx
+  std::uint32_t m, ncols;
 };
 
-__global__ void __launch_bounds__(256) gen_near(const double* __restrict__ pts, const KernelParams kp,
-                                                const std::uint32_t* __restrict__ perm,
-                                                const NearBlock* __restrict__ blocks, std::uint64_t nblocks,
-                                                double* __restrict__ dgen) {
+__global__ void __launch_bounds__(256) gen_blocks(const double* __restrict__ pts, const KernelParams kp,
+                                                  const std::uint32_t* __restrict__ idx,
+                                                  const GenBlock* __restrict__ blocks, std::uint64_t nblocks,
+                                                  double* __restrict__ out) {
   for (std::uint64_t s = blockIdx.x; s < nblocks; s += gridDim.x) {
-    const NearBlock b = blocks[s];
-    const std::uint32_t count = b.m_i * b.m_j;
+    const GenBlock b = blocks[s];
+    const std::uint32_t count = b.m * b.ncols;
     for (std::uint32_t e = threadIdx.x; e < count; e += blockDim.x) {
-      const std::uint32_t a = e % b.m_i, c = e / b.m_i;  // consecutive threads: consecutive rows
-      const std::uint64_t pi = perm[b.start_i + a], pj = perm[b.start_j + c];
-      dgen[b.off + e] = kernel_value(kp, pts + pi * kp.d, pts + pj * kp.d);
+      const std::uint32_t a = e % b.m, c = e / b.m;  // consecutive threads: consecutive rows
+      const std::uint64_t pi = idx[b.rows + a], pj = idx[b.cols + c];
+      out[b.off + e] = kernel_value(kp, pts + pi * kp.d, pts + pj * kp.d);
     }
   }
 }

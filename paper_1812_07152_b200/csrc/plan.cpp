@@ -30,7 +30,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     return fail(err, "cds: null array in view");
   if ((v.num_near && !v.near_pairs) || (v.num_far && !v.far_pairs) || (v.num_v && !v.v_order))
     return fail(err, "cds: null pair list in view");
-  if ((v.dptr[v.num_near] && !v.dgen && !split.generated_near) || (v.bptr[v.num_far] && !v.bgen) || (v.vptr[v.num_v] && !v.vgen))
+  if ((v.dptr[v.num_near] && !v.dgen && !split.generated_near) || (v.bptr[v.num_far] && !v.bgen && !split.generated_far) || (v.vptr[v.num_v] && !v.vgen))
     return fail(err, "cds: null generator array in view");
   if (v.n == 0 || v.n > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: point count out of range");

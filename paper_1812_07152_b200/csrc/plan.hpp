@@ -126,6 +126,7 @@ struct SplitSpec {
   std::uint32_t nparts = 1;
   std::uint32_t part = 0;
   bool generated_near = false;  // dgen may be null: the near blocks are generated on the device
+  bool generated_far = false;   // bgen may be null: the far blocks are generated on the device
 };
 bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err,
                 const SplitSpec& split = {});

@@ -68,3 +68,27 @@ def test_gaussian_bases_match(n, d, mode, h, bacc):
     ri = oracle.RefInstance(oracle.RefInstanceSpec(n=n, d=d, mode=mode, tau=0.65, leaf=64, max_rank=64, seed=4,
                                                    kernel=0, h=h, bacc=bacc))
     _compare(ri, Kernel.gaussian(h), exact=False)
+
+
+@pytest.mark.parametrize("kernel,exact", [(1, True), (0, False)])
+def test_gpu_inspector_p2_end_to_end(kernel, exact):
+    """Tree, interactions and samples from the host; compression, every kernel block and
+    the evaluation on the B200: the result is the reference's own CDS evaluated."""
+    from paper_1812_07152_b200 import Evaluator
+    from paper_1812_07152_b200.compress import cds_from_bases, skeleton_csr
+
+    ri = oracle.RefInstance(oracle.RefInstanceSpec(n=3000, d=3, mode=0, tau=0.65, leaf=64, max_rank=48, seed=9,
+                                                   kernel=kernel, h=0.7, bacc=1e-6))
+    k = Kernel.inverse_distance() if kernel else Kernel.gaussian(0.7)
+    sp, si = ri.samples()
+    bases = gpu_compress(ri.points(), k, ri.cds, sp, si, 1e-6, 48)
+    cds = cds_from_bases(ri.cds, bases)
+    if exact:
+        assert np.array_equal(cds.vgen, ri.cds.vgen)
+    ev = Evaluator(cds, points=ri.points(), kernel=k, skeletons=skeleton_csr(bases))
+    w = oracle.random_matrix(3000, 16, 2)
+    y = ev.evaluate(w)
+    y_stored = Evaluator(ri.cds).evaluate(w)
+    if exact:
+        assert np.array_equal(y, y_stored)
+    assert oracle.rel_frob(y, ri.evaluate(w)) <= 1e-12
