@@ -3,16 +3,21 @@
 //  * tile_a: one-time (upload) re-layout of every GEMM A operand (V^T, V, B_ij, D_ij
 //    row tiles) into zero-padded, XOR-swizzled 64 x 16 FP64 chunks, so the main kernel
 //    streams A with one 8 KB bulk copy per chunk and reads it without bank conflicts.
-//  * grouped_gemm: warp-specialized, mbarrier-pipelined grouped FP64 GEMM. One CTA owns
-//    one (output row tile, 64-column block); its K loop walks the tile's segment list,
-//    so a whole far+downward sum or a whole leaf row (V_i S_i + sum_j D_ij Wp_j) is
-//    accumulated in registers and stored once (single writer, no atomics). A producer
-//    warp streams A chunks with cp.async.bulk and B tiles (rows of Wp/T/S, 16 x 64) with
-//    TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a kStages-deep ring; four consumer
-//    warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4 — tcgen05 has no f64 kind).
+//  * eval_dag: the whole-evaluation persistent launch. One CTA owns one (output row tile,
+//    64-column block) work item at a time, claimed in topological order; its K loop walks
+//    the tile's segment list, so a whole far+downward sum or a whole leaf row
+//    (V_i S_i + sum_j D_ij Wp_j) is accumulated in registers and stored once (single
+//    writer, no atomics). A producer lane streams A chunks with cp.async.bulk and B tiles
+//    (rows of Wp/T/S, 16 x 68, unswizzled: the 68-double pitch is conflict-free) with TMA
+//    (cp.async.bulk.tensor.2d) into a kStages-deep mbarrier ring; four consumer warps run
+//    mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4 — tcgen05 has no f64 kind).
+//    grouped_gemm is the same tile machinery, one launch per tree level (diagnostics, and
+//    the GEMM of the error oracle in krows.cu).
 //  * permute_in / permute_out: the permutation into and out of the padded tree order
 //    (executor.cpp:35-39, :245-254), fused with the transpose between the user's column-
-//    major W/Y and the point-major (Q-contiguous) internal buffers Wp/T/S/Yp.
+//    major W/Y and the point-major internal buffers Wp/T/S/Yp (column blocks kCbPitch apart).
+//  * gen_blocks: kernel blocks K(x_rows, x_cols) generated on the device (near field and
+//    far blocks of hmxg_upload_generated).
 #pragma once
 
 #include <cuda.h>
