@@ -251,6 +251,9 @@ def ours(args) -> None:
     spec, q_total = config(args.config)
     if args.q:
         q_total = args.q
+    if world > 1:  # every rank builds the same CDS: share the host cores instead of oversubscribing them
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        spec.threads = max(1, (os.cpu_count() or 1) // local_world)
     t0 = time.time()
     inst = build_instance(spec)
     cds = inst.cds
