@@ -324,6 +324,9 @@ def ours(args) -> None:
                 "peak_source": "measured FP64 DMMA peak on this pool (profiles/r01_fp64_peak.txt); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "algorithmic_flops_per_launch": dom_flops,
+                # the bases' unit rows are row copies, not multiply-adds: the kernel's flops
+                # above exclude them; `value` counts the reference's 2Q(2|V|+|B|+|D|)
+                "identity_row_flops_not_executed": max(0.0, flops_step / world - sum(p["flops_per_col"] for p in phase_info) * q),
                 "algorithmic_bytes_per_launch": pinfo["gen_bytes"] + pinfo["io_bytes_per_col"] * q}
     # diagnostic (untimed): the same evaluation as level-by-level launches, per-launch times
     with torch.cuda.stream(stream):

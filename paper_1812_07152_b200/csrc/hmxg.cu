@@ -41,6 +41,7 @@ struct DevState {
   Task* tasks = nullptr;
   SegDev* segs = nullptr;
   std::uint32_t* ipmap = nullptr;
+  std::uint32_t* idmap = nullptr;  // identity-row sources of the tasks (Plan::idmap)
   std::size_t cap_q = 0;  // row pitch of Wp/T/S/Yp in physical columns (phys_cols of the capacity)
   double* wp = nullptr;
   double* yp = nullptr;
@@ -128,6 +129,8 @@ struct DevState {
     cudaFree(tasks);
     cudaFree(segs);
     cudaFree(ipmap);
+    cudaFree(idmap);
+    idmap = nullptr;
     tiles = nullptr;
     tasks = nullptr;
     segs = nullptr;
@@ -273,6 +276,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   p.ld[kBufS] = ldq;
   p.ld[kBufYp] = ldq;
   p.segs = d.segs;
+  p.idmap = d.idmap;
   p.q = qq;
   if (!levels) {
     const DevState::DagItems* di = nullptr;
@@ -517,11 +521,13 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
     HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
     HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
+    std::uint32_t* maps = nullptr;
+    HMXG_TRY(dev_upload(&maps, plan.maps.data(), plan.maps.size(), d.comp));
     if (plan.tile_elems) {
       HMXG_CUDA(cudaMalloc(&d.tiles, plan.tile_elems * sizeof(double)));
       const std::uint64_t nch = plan.chunk_seg.size();
       tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
-                                                                                               d.tiles, nch);
+                                                                                               maps, d.tiles, nch);
       HMXG_CUDA(cudaGetLastError());
     }
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
@@ -530,14 +536,16 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     cudaFree(gv);
     cudaFree(srcs);
     cudaFree(cseg);
+    cudaFree(maps);
     HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
     HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.idmap, plan.idmap.data(), plan.idmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
     d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
-                       4 * plan.ipmap.size();
+                       4 * plan.ipmap.size() + 4 * plan.idmap.size();
   }
   *out = mat.release();
   return HMXG_OK;
@@ -667,6 +675,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   p.tiles = d.tiles;
   p.tasks = d.tasks;
   p.segs = d.segs;
+  p.idmap = d.idmap;
   p.buf[kBufWp] = d.wp;
   p.buf[kBufT] = d.t;
   p.buf[kBufS] = d.s;

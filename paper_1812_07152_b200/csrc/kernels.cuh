@@ -69,6 +69,7 @@ struct GemmParams {
   double* buf[kNumBufs];        // Wp, T, S, Yp
   std::uint64_t ld[kNumBufs];
   std::uint32_t q;
+  const std::uint32_t* idmap;   // identity-row sources of the tasks (Task::id_off)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) gen_blocks(const double* __restrict__ pts
 // ---------------------------------------------------------------- A pre-tiling
 __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
                        const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,
-                       double* __restrict__ tiles, std::uint64_t nchunks) {
+                       const std::uint32_t* __restrict__ maps, double* __restrict__ tiles, std::uint64_t nchunks) {
   for (std::uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const TileSrc s = srcs[chunk_seg[c]];
     const std::uint64_t chunk_in_seg = (c * kChunkElems - s.tile_off) / kChunkElems;
@@ -187,8 +188,11 @@ __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__
       }
       const std::uint64_t kk = chunk_in_seg * kBK + k;
       double v = 0.0;
-      if (r < s.m && kk < s.k)
-        v = s.trans ? a[kk + static_cast<std::uint64_t>(r) * s.lda] : a[r + kk * s.lda];
+      if (r < s.m && kk < s.k) {
+        const std::uint64_t rs = s.rmap == kNoMap ? s.r0 + r : maps[s.rmap + s.r0 + r];
+        const std::uint64_t ks = s.kmap == kNoMap ? kk : maps[s.kmap + kk];
+        v = s.trans ? a[ks + rs * s.lda] : a[rs + ks * s.lda];
+      }
       out[a_swz(k, r)] = v;
     }
   }
@@ -378,17 +382,18 @@ __device__ __forceinline__ FragAddr frag_addresses(int wm, int wn, int fr, int f
 }
 
 // Consumers: the K loop and epilogue of one GEMM tile (each element stored exactly once).
+// `wait_id(task)` runs before the identity rows are read (the DAG kernel's wait for the
+// nodes that produce them; a no-op per level, where they ran in an earlier launch).
+template <class WaitId>
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
-                                                  std::uint32_t cb, const FragAddr& fa, std::uint32_t& it) {
+                                                  std::uint32_t cb, const FragAddr& fa, std::uint32_t& it,
+                                                  WaitId&& wait_id) {
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
-  std::uint32_t nchunks = 0;
-  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) nchunks += p.segs[si].nchunks;
-  // Warp-uniform trim of fragments outside the task's valid rows / the last column block.
+  // Warp-uniform trim of fragments outside the valid rows / the last column block.
   const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
-  const int frag_rows = (static_cast<int>(task.m) + 7) / 8, frag_cols = (static_cast<int>(ncols) + 7) / 8;
-  const int live_i = min(4, max(0, (frag_rows - wm + 1) / 2));
+  const int frag_cols = (static_cast<int>(ncols) + 7) / 8;
   const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
 
   double acc[4][4][2];
@@ -397,19 +402,54 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
-  // uniformly, once per tile) to a K loop instantiated for their live fragment count.
-  const std::uint32_t base = smem_u32(c.stage);
-  if (live_j == 4) {
-    switch (live_i) {
-      case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
-      case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
-      case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
-      case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
-      default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it); break;
+  // Identity rows of the bases: the accumulator starts as the exact row copy from T
+  // (upward) or S (downward). The loads are issued before the K loop, so they are in
+  // flight while the first chunks arrive.
+  if (task.id_off != kNoMap) {
+    wait_id(task);
+    const double* B = pick_buf(p, task.id_buf);
+    const std::uint64_t ldb = pick_ld(p, task.id_buf);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (2 * i + wm) * 8 + fr;
+      if (row >= task.m) continue;
+      const std::uint32_t src = __ldg(p.idmap + task.id_off + row);
+      if (src == kNoMap) continue;
+      const double* srow = B + static_cast<std::uint64_t>(src) * ldb + cb * kCbPitch;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = (2 * j + wn) * 8 + 2 * fk;
+        if (col + 1 < static_cast<int>(ncols)) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(srow + col));
+          acc[i][j][0] = v.x;
+          acc[i][j][1] = v.y;
+        } else if (col < static_cast<int>(ncols)) {
+          acc[i][j][0] = __ldcg(srow + col);
+        }
+      }
     }
-  } else {
-    consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nchunks, it, live_i, live_j);
+  }
+
+  // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
+  // uniformly, once per segment) to a K loop instantiated for their live fragment count.
+  // A segment may cover only the tile's first rows (SegDev::rows).
+  const std::uint32_t base = smem_u32(c.stage);
+  for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
+    const SegDev sg = p.segs[si];
+    const int rows = sg.rows ? static_cast<int>(sg.rows) : static_cast<int>(task.m);
+    const int live_i = min(4, max(0, ((rows + 7) / 8 - wm + 1) / 2));
+    const std::uint32_t nch = sg.nchunks;
+    if (live_j == 4) {
+      switch (live_i) {
+        case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+        case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+        case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+        case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+        default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+      }
+    } else {
+      consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nch, it, live_i, live_j);
+    }
   }
 
   double* C = pick_buf(p, task.cbuf);
@@ -465,7 +505,8 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   for (std::uint32_t seq = 0;; ++seq) {
     const std::uint64_t t = take_item(c, seq);
     if (t >= ntiles) break;
-    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks), fa, it);
+    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks), fa, it,
+                      [](const Task&) {});  // the copied rows' level ran in an earlier launch
   }
 }
 
@@ -559,7 +600,17 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
     const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-    consume_gemm_tile(p, c, task, cb, fa, it);
+    consume_gemm_tile(p, c, task, cb, fa, it, [&](const Task& t) {
+      // the nodes whose rows are copied are complete for this column block; every lane
+      // acquires, the copies are plain (L2) loads
+      for (const std::uint32_t node : {t.id_node0, t.id_node1}) {
+        if (node == kNoMap) continue;
+        const std::uint32_t* ctr = (t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb;
+        if (lane == 0) spin_until(ctr, d.node_tiles[node] * kConsumerWarps);
+        __syncwarp();
+        (void)ld_acquire(ctr);
+      }
+    });
     if (task.cbuf != kBufYp)  // leaf rows (Yp) have no dependent inside the launch
       warp_signal((task.cbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(task.node) * d.ncb + cb);
   }

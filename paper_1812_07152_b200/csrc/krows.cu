@@ -265,6 +265,7 @@ int kernel_rows_dev(hmxg_points& P, const std::uint32_t* rows, std::uint64_t nro
     for (std::uint32_t s = 0; s < S; ++s)
       for (std::uint32_t t = 0; t < ntr; ++t) {
         Task tk{};
+        tk.id_off = tk.id_node0 = tk.id_node1 = kNoMap;
         tk.c_row = (s * ntr + t) * kBM;
         tk.cbuf = kBufYp;
         tk.m = static_cast<std::uint16_t>(std::min<std::uint32_t>(kBM, nb - t * kBM));

@@ -162,6 +162,11 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   for (std::uint32_t i = 0; i < nn; ++i)
     if (active(i)) plan.node_tiles[i] = (v.sranks[i] + bm - 1) / bm;
   std::uint32_t cur_node = 0;
+  // identity sources of the current node's output rows (row -> absolute row of id_buf, or
+  // kNoMap), set by the pass before add_tiles; empty: none
+  std::vector<std::uint32_t> cur_id;
+  std::uint16_t cur_id_buf = 0;
+  std::uint32_t cur_id_node0 = kNoMap, cur_id_node1 = kNoMap;
   auto add_tiles = [&](std::uint32_t m, Buf cbuf, std::uint64_t c_row, auto&& emit_segs, Phase& ph) {
     const std::uint32_t tiles = m == 0 ? 0 : (m + bm - 1) / bm;
     if (cbuf == kBufYp) plan.leaf_tasks += tiles;
@@ -172,13 +177,26 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       task.cbuf = cbuf;
       task.m = static_cast<std::uint16_t>(std::min(bm, m - r0));
       task.node = cur_node;
+      task.id_off = kNoMap;
+      task.id_node0 = task.id_node1 = kNoMap;
       task.seg_begin = static_cast<std::uint32_t>(plan.segs.size());
       emit_segs(r0, task.m);
       task.seg_end = static_cast<std::uint32_t>(plan.segs.size());
+      if (!cur_id.empty()) {
+        bool any = false;
+        for (std::uint32_t r = r0; r < r0 + task.m; ++r) any = any || cur_id[r] != kNoMap;
+        if (any) {
+          task.id_off = static_cast<std::uint32_t>(plan.idmap.size());
+          plan.idmap.insert(plan.idmap.end(), cur_id.begin() + r0, cur_id.begin() + r0 + task.m);
+          task.id_buf = cur_id_buf;
+          task.id_node0 = cur_id_node0;
+          task.id_node1 = cur_id_node1;
+        }
+      }
       for (std::uint32_t s = task.seg_begin; s < task.seg_end; ++s) {
-        const double k = plan.tile_src[s].k;
-        ph.flops_per_col += 2.0 * task.m * k;
-        ph.gen_bytes += 8.0 * task.m * k;
+        const double k = plan.tile_src[s].k, rows = plan.tile_src[s].m;
+        ph.flops_per_col += 2.0 * rows * k;  // executed: identity rows are row copies
+        ph.gen_bytes += 8.0 * rows * k;
         if (t == 0) ph.io_bytes_per_col += 8.0 * k;  // B rows, read once per node
       }
       plan.tasks.push_back(task);
@@ -186,22 +204,30 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     ph.io_bytes_per_col += 8.0 * m;  // C rows, written once
     plan.max_m = std::max(plan.max_m, m);
   };
-  // A operand rows [r0, r0+m) of the generator block at a_off; K columns; B rows b_row.
+  // A operand of one segment: tile rows r < m read generator row rmap[r0 + r] (or r0 + r),
+  // K index k < kcount reads generator column kmap[k] (or k), of the block at a_off with
+  // leading dimension lda; B rows [b_row, b_row + kcount). Only the first `rows` tile rows
+  // carry data (the rest are identity rows handled as row copies, zero in A).
   auto push_seg = [&](Gen gen, bool trans, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k,
-                      std::uint32_t m, Buf bbuf, std::uint64_t b_row, std::uint32_t src = 0) {
-    if (k == 0) return;
+                      std::uint32_t m, Buf bbuf, std::uint64_t b_row, std::uint32_t src, std::uint32_t r0,
+                      std::uint32_t rmap, std::uint32_t kmap, std::uint32_t rows) {
+    rows = std::min(rows, m);
+    if (k == 0 || rows == 0) return;
     const std::uint64_t chunks = (k + kRowAlign - 1) / kRowAlign;
     TileSrc ts{};
     ts.a_off = a_off;
     ts.tile_off = plan.tile_elems;
     ts.lda = static_cast<std::uint32_t>(lda);
     ts.k = static_cast<std::uint32_t>(k);
-    ts.m = static_cast<std::uint16_t>(m);
+    ts.m = static_cast<std::uint16_t>(rows);
     ts.gen = gen;
     ts.trans = trans ? 1 : 0;
+    ts.r0 = r0;
+    ts.rmap = rmap;
+    ts.kmap = kmap;
     for (std::uint64_t c = 0; c < chunks; ++c) plan.chunk_seg.push_back(static_cast<std::uint32_t>(plan.segs.size()));
-    plan.segs.push_back(SegDev{plan.tile_elems, static_cast<std::uint32_t>(b_row),
-                               static_cast<std::uint16_t>(chunks), static_cast<std::uint16_t>(bbuf), src, 0});
+    plan.segs.push_back(SegDev{plan.tile_elems, static_cast<std::uint32_t>(b_row), static_cast<std::uint16_t>(chunks),
+                               static_cast<std::uint16_t>(bbuf), src, rows < m ? rows : 0});
     plan.tile_src.push_back(ts);
     plan.tile_elems += chunks * kRowAlign * bm;
   };
@@ -230,6 +256,64 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   auto mine = [&](std::uint32_t i) { return !splitting || owner[i] == me; };
   auto top = [&](std::uint32_t i) { return splitting && owner[i] < 0; };
 
+  // --- identity rows of the bases. An interpolative basis V_p has a unit row for every
+  // skeleton column (compress.cpp:79-81: V(piv[j], j) = 1, the rest of the row 0), so the
+  // rows of a child c that the parent keeps contribute exact row copies: T_p(j) += T_c(row)
+  // upward and S_c(row) += S_p(j) downward. Each active child's rows (its T and S order,
+  // the columns of its V, the rows / columns of its far blocks) are reordered as
+  // [rows dense in V_p, rows copied by V_p]: the upward K range of the child is then a
+  // prefix and the downward V_p product covers a prefix of the child's rows. The copies
+  // move to the tile epilogue; only multiply-adds by exact zeros and ones are dropped.
+  std::vector<std::vector<std::uint32_t>> rperm(nn);  // node row order: new -> old (empty: identity)
+  std::vector<std::vector<std::uint32_t>> rpos(nn);   // old -> new
+  std::vector<std::vector<std::uint32_t>> idcol(nn);  // old row -> parent column it copies (kNoMap)
+  std::vector<std::vector<std::uint64_t>> colsrc(nn); // parent: column -> (child << 32 | old row), or ~0
+  std::vector<std::uint32_t> dense(nn, 0);            // rows [0, dense) of a node are dense in V_parent
+  std::vector<std::uint32_t> map_off(nn, kNoMap);
+  for (std::uint32_t i = 0; i < nn; ++i) dense[i] = v.sranks[i];
+  if (split.identity_rows && v.num_v) {
+    for (std::uint32_t p = 0; p < nn; ++p) {
+      if (!active(p) || is_leaf(p)) continue;
+      const std::uint32_t lc = v.lchild[p], rc = v.rchild[p];
+      const std::uint64_t W = v_width(p), K = v.sranks[p], klc = v.sranks[lc];
+      const double* V = v.vgen + v.vptr[vslot[p]];
+      colsrc[p].assign(K, ~std::uint64_t(0));
+      for (std::uint32_t c : {lc, rc}) idcol[c].assign(v.sranks[c], kNoMap);
+      for (std::uint64_t r = 0; r < W; ++r) {
+        std::uint64_t nz = 0, col = 0;
+        for (std::uint64_t j = 0; j < K && nz < 2; ++j)
+          if (V[r + j * W] != 0.0) {
+            ++nz;
+            col = j;
+          }
+        if (nz != 1 || V[r + col * W] != 1.0 || colsrc[p][col] != ~std::uint64_t(0)) continue;
+        const std::uint32_t c = r < klc ? lc : rc;
+        const std::uint32_t old = static_cast<std::uint32_t>(r < klc ? r : r - klc);
+        idcol[c][old] = static_cast<std::uint32_t>(col);
+        colsrc[p][col] = (std::uint64_t(c) << 32) | old;
+      }
+      for (std::uint32_t c : {lc, rc}) {
+        if (!active(c)) continue;
+        std::vector<std::uint32_t>& order_c = rperm[c];
+        for (std::uint32_t r = 0; r < v.sranks[c]; ++r)
+          if (idcol[c][r] == kNoMap) order_c.push_back(r);
+        dense[c] = static_cast<std::uint32_t>(order_c.size());
+        for (std::uint32_t r = 0; r < v.sranks[c]; ++r)
+          if (idcol[c][r] != kNoMap) order_c.push_back(r);
+        if (dense[c] == v.sranks[c]) {  // nothing copied: keep the natural order
+          order_c.clear();
+          continue;
+        }
+        rpos[c].assign(v.sranks[c], 0);
+        for (std::uint32_t q = 0; q < v.sranks[c]; ++q) rpos[c][order_c[q]] = q;
+        map_off[c] = static_cast<std::uint32_t>(plan.maps.size());
+        plan.maps.insert(plan.maps.end(), order_c.begin(), order_c.end());
+      }
+    }
+  }
+  auto oldrow = [&](std::uint32_t i, std::uint32_t r) { return rperm[i].empty() ? r : rperm[i][r]; };
+  auto newrow = [&](std::uint32_t i, std::uint32_t r) { return rpos[i].empty() ? r : rpos[i][r]; };
+
   std::uint32_t cur_stage = 0;
   auto open_phase = [&](PhaseKind kind, std::uint32_t level) {
     plan.phases.push_back(
@@ -252,17 +336,33 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         const std::uint64_t lda = v_width(i);
         const std::uint64_t vo = v.vptr[vslot[i]];
         cur_node = i;
+        cur_id.clear();
+        cur_id_node0 = cur_id_node1 = kNoMap;
+        if (!is_leaf(i) && !colsrc[i].empty()) {  // T_i(j) += T_child(copied row)
+          cur_id.assign(v.sranks[i], kNoMap);
+          for (std::uint32_t r = 0; r < v.sranks[i]; ++r) {
+            const std::uint64_t src = colsrc[i][oldrow(i, r)];
+            if (src == ~std::uint64_t(0)) continue;
+            const std::uint32_t c = static_cast<std::uint32_t>(src >> 32), old = static_cast<std::uint32_t>(src);
+            cur_id[r] = static_cast<std::uint32_t>(plan.node_off[c] + newrow(c, old));
+          }
+          cur_id_buf = kBufT;
+          cur_id_node0 = active(v.lchild[i]) ? v.lchild[i] : kNoMap;
+          cur_id_node1 = active(v.rchild[i]) ? v.rchild[i] : kNoMap;
+        }
         add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
+          // A = V_i^T: tile row r is column oldrow(i, r) of V_i
           if (is_leaf(i)) {
-            push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, lda, m, kBufWp, plan.leaf_row[i]);
+            push_seg(kGenV, true, vo, lda, lda, m, kBufWp, plan.leaf_row[i], 0, r0, map_off[i], kNoMap, m);
           } else {
             const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
             const std::uint64_t srl = v.sranks[lc];
+            // K: the child's dense rows (a prefix of its order); copied rows are epilogue adds
             if (active(lc))
-              push_seg(kGenV, true, vo + std::uint64_t(r0) * lda, lda, srl, m, kBufT, plan.node_off[lc], lc);
+              push_seg(kGenV, true, vo, lda, dense[lc], m, kBufT, plan.node_off[lc], lc, r0, map_off[i], map_off[lc], m);
             if (active(rc))
-              push_seg(kGenV, true, vo + std::uint64_t(r0) * lda + srl, lda, v.sranks[rc], m, kBufT,
-                       plan.node_off[rc], rc);
+              push_seg(kGenV, true, vo + srl, lda, dense[rc], m, kBufT, plan.node_off[rc], rc, r0, map_off[i],
+                       map_off[rc], m);
           }
         }, plan.phases.back());
       }
@@ -281,15 +381,26 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       if (v.level[c] != d || !active(c) || !(mine(c) || top(c))) continue;
       const std::uint32_t p = v.parent[c];
       cur_node = c;
+      cur_id.clear();
+      cur_id_node0 = cur_id_node1 = kNoMap;
+      if (p != HMXG_NO_NODE && active(p) && !rperm[c].empty()) {  // S_c(row) += S_p(copied column)
+        cur_id.assign(v.sranks[c], kNoMap);
+        for (std::uint32_t r = dense[c]; r < v.sranks[c]; ++r)
+          cur_id[r] = static_cast<std::uint32_t>(plan.node_off[p] + newrow(p, idcol[c][oldrow(c, r)]));
+        cur_id_buf = kBufS;
+        cur_id_node0 = p;
+      }
       add_tiles(v.sranks[c], kBufS, plan.node_off[c], [&](std::uint32_t r0, std::uint32_t m) {
         for (std::uint64_t s : far_of[c]) {
           const std::uint32_t j = v.far_pairs[2 * s + 1];
-          push_seg(kGenB, false, v.bptr[s] + r0, v.sranks[c], v.sranks[j], m, kBufT, plan.node_off[j], j);
+          push_seg(kGenB, false, v.bptr[s], v.sranks[c], v.sranks[j], m, kBufT, plan.node_off[j], j, r0, map_off[c],
+                   map_off[j], m);
         }
         if (p != HMXG_NO_NODE && active(p)) {
           const std::uint64_t row_in_parent = (c == v.lchild[p]) ? 0 : v.sranks[v.lchild[p]];
-          push_seg(kGenV, false, v.vptr[vslot[p]] + row_in_parent + r0, v_width(p), v.sranks[p], m, kBufS,
-                   plan.node_off[p], p);
+          const std::uint32_t rows = dense[c] > r0 ? dense[c] - r0 : 0;  // the copied rows sit below
+          push_seg(kGenV, false, v.vptr[vslot[p]] + row_in_parent, v_width(p), v.sranks[p], m, kBufS,
+                   plan.node_off[p], p, r0, map_off[c], map_off[p], rows);
         }
       }, plan.phases.back());
     }
@@ -302,11 +413,15 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     if (!is_leaf(i) || !mine(i)) continue;
     const std::uint32_t m = size_of(i);
     cur_node = i;
+    cur_id.clear();
+    cur_id_node0 = cur_id_node1 = kNoMap;
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
-      if (active(i)) push_seg(kGenV, false, v.vptr[vslot[i]] + r0, m, v.sranks[i], mt, kBufS, plan.node_off[i], i);
+      if (active(i))
+        push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, kNoMap, map_off[i],
+                 mt);
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
-        push_seg(kGenD, false, v.dptr[s] + r0, m, size_of(j), mt, kBufWp, plan.leaf_row[j]);
+        push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, kNoMap, kNoMap, mt);
       }
     }, plan.phases.back());
   }

@@ -39,7 +39,11 @@ enum Gen : std::uint8_t { kGenD = 0, kGenB = 1, kGenV = 2 };
 
 // Source of one pre-tiled A operand: rows [0, m) of the tile, K columns, from generator
 // `gen` at element offset a_off, column major with leading dimension lda; with `trans`
-// the stored matrix is A^T (A(r,k) = a[k + r*lda]). Tiled to tile_off (in doubles).
+// the stored matrix is A^T (A(r,k) = a[k + r*lda]). Tile row r reads generator row
+// rmap[r0 + r] and K index k reads generator column kmap[k] (the node row orders of the
+// identity-row lowering, Plan::maps), or r0 + r and k without a map (kNoMap). Tiled to
+// tile_off (in doubles).
+constexpr std::uint32_t kNoMap = 0xffffffffu;
 struct TileSrc {
   std::uint64_t a_off;
   std::uint64_t tile_off;
@@ -48,26 +52,34 @@ struct TileSrc {
   std::uint16_t m;
   std::uint8_t gen;
   std::uint8_t trans;
+  std::uint32_t r0;
+  std::uint32_t rmap;
+  std::uint32_t kmap;
   std::uint32_t pad;
 };
-static_assert(sizeof(TileSrc) == 32, "TileSrc layout");
+static_assert(sizeof(TileSrc) == 48, "TileSrc layout");
 
 // One K segment of a task as the GEMM kernel sees it: nchunks pre-tiled A chunks at
 // tile_off, and B rows [b_row, b_row + 16*nchunks) of buffer bbuf.
 // `src` is the node whose T or S rows the segment reads (the DAG kernel waits for that
-// node's tiles of the same column block); unused for Wp.
+// node's tiles of the same column block); unused for Wp. `rows`: the segment only
+// contributes to the tile's first `rows` output rows (its A operand is zero below), so
+// fragments below are not multiplied.
 struct SegDev {
   std::uint64_t tile_off;
   std::uint32_t b_row;
   std::uint16_t nchunks;
   std::uint16_t bbuf;
   std::uint32_t src;
-  std::uint32_t pad;
+  std::uint32_t rows;
 };
 static_assert(sizeof(SegDev) == 24, "SegDev layout");
 
 // One output row tile: rows [c_row, c_row + m) of buffer cbuf, all columns (grid.y).
 // `node` owns the output rows (T or S of that node; Yp for a leaf).
+// Identity rows (the interpolative bases' unit rows): when id_off != kNoMap, output row r
+// also adds row idmap[id_off + r] of buffer id_buf (kNoMap: nothing), whose producers are
+// the nodes id_node0 / id_node1 (kNoMap: none) the DAG consumer waits for first.
 struct Task {
   std::uint32_t c_row;
   std::uint16_t cbuf;
@@ -75,9 +87,14 @@ struct Task {
   std::uint32_t seg_begin;
   std::uint32_t seg_end;
   std::uint32_t node;
-  std::uint32_t pad;
+  std::uint32_t id_off;
+  std::uint32_t id_node0;
+  std::uint32_t id_node1;
+  std::uint16_t id_buf;
+  std::uint16_t pad0;
+  std::uint32_t pad1;
 };
-static_assert(sizeof(Task) == 24, "Task layout");
+static_assert(sizeof(Task) == 40, "Task layout");
 
 enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2 };
 
@@ -113,6 +130,11 @@ struct Plan {
   std::uint32_t leaf_tasks = 0;           // row tiles of the leaf (Yp) phase
   std::uint64_t d_elems = 0, b_elems = 0, v_elems = 0;
   std::uint32_t max_m = 0;
+  // identity-row lowering (plan.cpp): node row orders (TileSrc rmap/kmap index them) and
+  // the per-row identity sources of tasks (Task::id_off indexes them)
+  std::vector<std::uint32_t> maps;
+  std::vector<std::uint32_t> idmap;
+  double identity_flops_per_col = 0.0;  // multiply-adds by exact 0/1 rows the kernel skips
 };
 
 // Validates the view (structure.hpp invariants the evaluator relies on) and lowers it.
@@ -125,6 +147,7 @@ struct Plan {
 struct SplitSpec {
   std::uint32_t nparts = 1;
   std::uint32_t part = 0;
+  bool identity_rows = true;    // lower the bases' unit rows to row copies (plan.cpp)
   bool generated_near = false;  // dgen may be null: the near blocks are generated on the device
   bool generated_far = false;   // bgen may be null: the far blocks are generated on the device
 };
