@@ -25,7 +25,7 @@ HMXG_F_NO_SYNC = 0x2
 HMXG_F_TIME_PHASES = 0x4
 HMXG_F_NO_GRAPH = 0x8
 HMXG_F_LEVEL_LAUNCHES = 0x10
-PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter", 5: "dag"}
+PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter", 5: "dag", 6: "near"}
 
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)

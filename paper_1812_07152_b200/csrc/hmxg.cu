@@ -64,6 +64,7 @@ struct DevState {
   std::uint32_t* dag_done = nullptr;  // claim counter + done counters (sized for the largest q)
   std::size_t dag_done_cap = 0;
   std::uint32_t* node_tiles = nullptr;
+  std::uint32_t* yp_tiles = nullptr;
   std::uint32_t* remote_t = nullptr;  // split mode: nodes whose T comes from the exchange
   // CUDA graph of the whole launch sequence for one (W, Y, q, ld, stream, workspace) key:
   // repeated device-pointer evaluations replay it instead of issuing ~2H+4 launches.
@@ -81,6 +82,7 @@ struct DevState {
   } gkey;
   cudaGraphExec_t gexec = nullptr;
   bool last_levels = false;  // launch sequence of the last evaluation (phase reporting)
+  std::size_t last_q = 0;    // its column count (per device shard)
   std::uint32_t glaunches = 0;
   unsigned gemm_grid = 0;                   // resident CTAs of the persistent GEMM
 
@@ -121,6 +123,8 @@ struct DevState {
     }
     cudaFree(dag_done);
     cudaFree(node_tiles);
+    cudaFree(yp_tiles);
+    yp_tiles = nullptr;
     cudaFree(remote_t);
     remote_t = nullptr;
     dag_done = nullptr;
@@ -191,24 +195,74 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 }
 
 // Work items of the whole-evaluation DAG launch for q columns, in topological order:
-// levels in launch order (upward by height, far+downward by depth, leaves), each level's
-// row tiles in task order with the column block fastest (so a row tile's A chunks are
-// re-served from L2 to all column blocks).
+// within a phase, row tiles in task order with the column block fastest (so a row tile's A
+// chunks are re-served from L2 to all column blocks).
+// With few column blocks the tree levels are too narrow to keep every SM busy, and the
+// split leaf variant is used: its near phase depends on Wp only, so its items are dealt
+// out in equal slices after every tree level but the first (CTAs that would wait for the
+// next level pick up near-field tiles instead), and the accumulating leaf phase comes
+// last. With many column blocks the Yp round trip of the split costs more than the idle
+// slots it fills (cfg5-HSS at Q=2048: +11% DAG time), so the combined leaf tasks run.
+constexpr std::uint32_t kSplitLeafMaxBlocks = 4;
+bool split_leaf(const Plan& plan, std::size_t q) {
+  return (q + kBN - 1) / kBN <= kSplitLeafMaxBlocks && !plan.split_phases.empty();
+}
+// The level-by-level launch sequence for q columns (HMXG_F_LEVEL_LAUNCHES): the same leaf
+// variant as the DAG launch, so both give the same bits.
+std::vector<const Phase*> level_phases(const Plan& plan, std::size_t q) {
+  std::vector<const Phase*> out;
+  const bool split = split_leaf(plan, q);
+  for (const Phase& ph : plan.phases)
+    if (!(split && ph.kind == kPhaseLeaf)) out.push_back(&ph);
+  if (split)
+    for (const Phase& ph : plan.split_phases) out.push_back(&ph);
+  return out;
+}
 std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
   std::vector<std::uint64_t> items;
-  for (const Phase& ph : plan.phases)
-    if (ph.stage == stage)
-    for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+  auto emit = [&](std::uint32_t t0, std::uint32_t t1) {
+    for (std::uint32_t t = t0; t < t1; ++t)
       for (std::uint32_t cb = 0; cb < ncb; ++cb) items.push_back(make_item(kItemGemm, cb, t));
+  };
+  const bool split = split_leaf(plan, q);
+  std::vector<const Phase*> tree, leaf;
+  const Phase* near = nullptr;
+  for (const Phase& ph : plan.phases) {
+    if (ph.stage != stage) continue;
+    if (ph.kind == kPhaseLeaf) {
+      if (!split) leaf.push_back(&ph);
+    } else {
+      tree.push_back(&ph);
+    }
+  }
+  if (split)
+    for (const Phase& ph : plan.split_phases) {
+      if (ph.stage != stage) continue;
+      if (ph.kind == kPhaseNear) near = &ph;
+      else leaf.push_back(&ph);
+    }
+  const std::uint64_t nt = near ? near->task_end - near->task_begin : 0;
+  const std::size_t L = tree.size();
+  const std::size_t nslices = L > 1 ? L - 1 : 1;  // after every level but the first
+  for (std::size_t k = 0; k < L; ++k) {
+    emit(tree[k]->task_begin, tree[k]->task_end);
+    if (near && (L == 1 || k >= 1)) {
+      const std::size_t slice = L == 1 ? 0 : k - 1;
+      emit(near->task_begin + static_cast<std::uint32_t>(nt * slice / nslices),
+           near->task_begin + static_cast<std::uint32_t>(nt * (slice + 1) / nslices));
+    }
+  }
+  if (near && L == 0) emit(near->task_begin, near->task_end);
+  for (const Phase* ph : leaf) emit(ph->task_begin, ph->task_end);
   return items;
 }
 
-// [claim counter per stage | T counters (nodes x ncb) | S counters (nodes x ncb)]
+// [claim counter per stage | T counters | S counters | Yp counters] (nodes x ncb each)
 constexpr std::size_t kDagClaimWords = 2;
 std::size_t dag_done_words(const Plan& plan, std::size_t q) {
   const std::size_t ncb = (q + kBN - 1) / kBN;
-  return kDagClaimWords + 2 * std::size_t(plan.num_nodes) * ncb;
+  return kDagClaimWords + 3 * std::size_t(plan.num_nodes) * ncb;  // T, S, Yp counters
 }
 
 // Item list and counters for q columns (built on first use, cached for a few q).
@@ -249,6 +303,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   const std::uint32_t n = static_cast<std::uint32_t>(plan.n);
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
   const dim3 eblk(256);
+  d.last_q = q;
   // Per-launch timing events. Under graph capture they become external event-record
   // nodes, so a replayed graph still times every launch.
   std::size_t ev = 0;
@@ -289,6 +344,8 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.claim = d.dag_done;
     dp.done = d.dag_done + kDagClaimWords;
     dp.node_tiles = d.node_tiles;
+  dp.yp_tiles = d.yp_tiles;
+    dp.yp_tiles = d.yp_tiles;
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
     p.tasks = d.tasks;
@@ -317,9 +374,10 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   ++*launches;
   HMXG_TRY(mark());
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
-  HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, plan.phases.size() * sizeof(std::uint32_t), st));
-  for (std::size_t ph_i = 0; ph_i < plan.phases.size(); ++ph_i) {
-    const Phase& ph = plan.phases[ph_i];
+  const std::vector<const Phase*> lphases = level_phases(plan, q);
+  HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, lphases.size() * sizeof(std::uint32_t), st));
+  for (std::size_t ph_i = 0; ph_i < lphases.size(); ++ph_i) {
+    const Phase& ph = *lphases[ph_i];
     p.tasks = d.tasks + ph.task_begin;
     const std::uint32_t ntasks = ph.task_end - ph.task_begin;
     const std::uint64_t tiles = std::uint64_t(ntasks) * col_blocks;
@@ -491,7 +549,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
         HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    d.phase_ev.resize(plan.phases.size() + 3);
+    d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     HMXG_CUDA(cudaFuncSetAttribute(eval_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -507,7 +565,8 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
 #define HMXG_GEMM_CTAS_PER_SM 3
 #endif
       d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
-      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size()) * sizeof(std::uint32_t)));
+      HMXG_CUDA(cudaMalloc(&d.tile_counters,
+                           std::max<std::size_t>(1, plan.phases.size() + plan.split_phases.size()) * sizeof(std::uint32_t)));
     }
     // raw generators -> pre-tiled A operands on the device, then the raw copies go away
     double *gd = nullptr, *gb = nullptr, *gv = nullptr;
@@ -542,6 +601,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&d.idmap, plan.idmap.data(), plan.idmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.yp_tiles, plan.yp_tiles.data(), plan.yp_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
     d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
@@ -688,6 +748,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.claim = d.dag_done + stage;
   dp.done = d.dag_done + kDagClaimWords;
   dp.node_tiles = d.node_tiles;
+  dp.yp_tiles = d.yp_tiles;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
   const dim3 pgrid((nn + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
@@ -764,19 +825,22 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
 // eval_dag, permute-out) by default, the level sequence after HMXG_F_LEVEL_LAUNCHES.
 int hmxg_phase_count(const hmxg_mat* mat) {
   if (!mat) return -1;
-  return mat->devs[0].last_levels ? static_cast<int>(mat->plan.phases.size() + 2) : 3;
+  const DevState& d = mat->devs[0];
+  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q).size() + 2) : 3;
 }
 
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
   const Plan& p = mat->plan;
   const bool levels = mat->devs[0].last_levels;
-  const std::uint32_t count = static_cast<std::uint32_t>(levels ? p.phases.size() + 2 : 3);
+  const std::vector<const Phase*> lphases = level_phases(p, mat->devs[0].last_q);
+  const std::uint32_t count = static_cast<std::uint32_t>(levels ? lphases.size() + 2 : 3);
   if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
   std::memset(out, 0, sizeof *out);
   if (!levels && idx == 1) {  // the whole-evaluation DAG launch: every GEMM tile
     out->kind = 5;
-    for (const Phase& ph : p.phases) {
+    for (const Phase* php : lphases) {
+      const Phase& ph = *php;
       out->tiles += ph.task_end - ph.task_begin;
       out->flops_per_col += ph.flops_per_col;
       out->gen_bytes += ph.gen_bytes;
@@ -788,8 +852,8 @@ int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
     out->io_bytes_per_col = 16.0 * p.n;
     out->gen_bytes = 4.0 * p.n;  // the permutation itself
   } else {
-    const Phase& ph = p.phases[idx - 1];
-    out->kind = ph.kind == kPhaseUp ? 1 : (ph.kind == kPhaseDown ? 2 : 3);
+    const Phase& ph = *lphases[idx - 1];
+    out->kind = ph.kind == kPhaseUp ? 1 : (ph.kind == kPhaseDown ? 2 : (ph.kind == kPhaseLeaf ? 3 : 6));
     out->level = ph.level;
     out->tiles = ph.task_end - ph.task_begin;
     out->flops_per_col = ph.flops_per_col;

@@ -406,14 +406,18 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
   // (upward) or S (downward). The loads are issued before the K loop, so they are in
   // flight while the first chunks arrive.
   if (task.id_off != kNoMap) {
+    std::uint32_t srcs[4];  // static sources: fetched while the producing nodes may still run
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (2 * i + wm) * 8 + fr;
+      srcs[i] = row < task.m ? __ldg(p.idmap + task.id_off + row) : kNoMap;
+    }
     wait_id(task);
     const double* B = pick_buf(p, task.id_buf);
     const std::uint64_t ldb = pick_ld(p, task.id_buf);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int row = (2 * i + wm) * 8 + fr;
-      if (row >= task.m) continue;
-      const std::uint32_t src = __ldg(p.idmap + task.id_off + row);
+      const std::uint32_t src = srcs[i];
       if (src == kNoMap) continue;
       const double* srow = B + static_cast<std::uint64_t>(src) * ldb + cb * kCbPitch;
 #pragma unroll
@@ -528,8 +532,9 @@ struct DagParams {
   const std::uint64_t* items;
   std::uint32_t nitems;
   std::uint32_t* claim;        // work-item counter (zeroed per evaluation)
-  std::uint32_t* done;         // [T: nodes*ncb | S: nodes*ncb] warp signals (zeroed)
+  std::uint32_t* done;         // [T: nodes*ncb | S: nodes*ncb | Yp: nodes*ncb] warp signals (zeroed)
   const std::uint32_t* node_tiles;
+  const std::uint32_t* yp_tiles;  // near-phase row tiles per leaf
   std::uint32_t ncb, nodes;
 };
 
@@ -570,6 +575,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   std::uint32_t* const done_t = d.done;
   std::uint32_t* const done_s = done_t + static_cast<std::uint64_t>(d.nodes) * d.ncb;
+  std::uint32_t* const done_y = done_s + static_cast<std::uint64_t>(d.nodes) * d.ncb;
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
@@ -605,14 +611,17 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       // acquires, the copies are plain (L2) loads
       for (const std::uint32_t node : {t.id_node0, t.id_node1}) {
         if (node == kNoMap) continue;
-        const std::uint32_t* ctr = (t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb;
-        if (lane == 0) spin_until(ctr, d.node_tiles[node] * kConsumerWarps);
+        const std::uint32_t* ctr = (t.id_buf == kBufT ? done_t : (t.id_buf == kBufS ? done_s : done_y)) +
+                                   static_cast<std::uint64_t>(node) * d.ncb + cb;
+        const std::uint32_t tiles = t.id_buf == kBufYp ? d.yp_tiles[node] : d.node_tiles[node];
+        if (lane == 0) spin_until(ctr, tiles * kConsumerWarps);
         __syncwarp();
         (void)ld_acquire(ctr);
       }
     });
-    if (task.cbuf != kBufYp)  // leaf rows (Yp) have no dependent inside the launch
-      warp_signal((task.cbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(task.node) * d.ncb + cb);
+    // Yp rows: the leaf phase accumulates onto the near phase's rows of the same leaf
+    warp_signal((task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
+                static_cast<std::uint64_t>(task.node) * d.ncb + cb);
   }
 }
 

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <limits>
 #include <sstream>
 
@@ -407,7 +408,17 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     close_phase();
   }
 
-  // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j (every leaf row written once)
+  // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j, one task per leaf row tile
+  //     (kPhaseLeaf, every leaf row written once; the V segment first, then the D ones).
+  //     The split variant (Plan::split_phases) runs the same D segments as a near task that
+  //     needs only Wp, and the V segment as a leaf task that accumulates onto the near rows
+  //     (identity rows from Yp): the DAG can then fill the tree passes' idle slots with
+  //     near-field tiles. Both variants share the segments and pre-tiled operands.
+  plan.yp_tiles.assign(nn, 0);
+  struct LeafTasks {
+    std::uint32_t node, t0, t1;  // combined tasks [t0, t1) in plan.tasks
+  };
+  std::vector<LeafTasks> leaf_tasks_of;
   open_phase(kPhaseLeaf, 0);
   for (std::uint32_t i : order) {
     if (!is_leaf(i) || !mine(i)) continue;
@@ -415,6 +426,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     cur_node = i;
     cur_id.clear();
     cur_id_node0 = cur_id_node1 = kNoMap;
+    const std::uint32_t t0 = static_cast<std::uint32_t>(plan.tasks.size());
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
       if (active(i))
         push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, kNoMap, map_off[i],
@@ -424,8 +436,58 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, kNoMap, kNoMap, mt);
       }
     }, plan.phases.back());
+    leaf_tasks_of.push_back({i, t0, static_cast<std::uint32_t>(plan.tasks.size())});
   }
   close_phase();
+  // split variant: near tasks, then leaf tasks accumulating onto them
+  const std::uint32_t near_begin = static_cast<std::uint32_t>(plan.tasks.size());
+  std::vector<std::uint8_t> split_leaf(nn, 0);
+  for (const LeafTasks& lt : leaf_tasks_of) {
+    const std::uint32_t i = lt.node;
+    if (active(i) && near_of[i].empty()) continue;  // V only: its leaf task below writes the rows
+    const bool with_v = active(i);
+    if (with_v) split_leaf[i] = 1;
+    plan.yp_tiles[i] = lt.t1 - lt.t0;
+    for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
+      Task nt = plan.tasks[t];
+      if (with_v) nt.seg_begin += 1;  // drop the V segment (the first of the task)
+      plan.tasks.push_back(nt);
+    }
+  }
+  const std::uint32_t near_end = static_cast<std::uint32_t>(plan.tasks.size());
+  for (const LeafTasks& lt : leaf_tasks_of) {
+    const std::uint32_t i = lt.node;
+    if (!active(i)) continue;
+    for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
+      Task vt = plan.tasks[t];
+      if (split_leaf[i]) {  // V segment only, accumulating onto the near rows of the tile
+        vt.seg_end = vt.seg_begin + 1;
+        vt.id_off = static_cast<std::uint32_t>(plan.idmap.size());
+        for (std::uint32_t r = 0; r < vt.m; ++r) plan.idmap.push_back(vt.c_row + r);
+        vt.id_buf = kBufYp;
+        vt.id_node0 = i;
+        vt.id_node1 = kNoMap;
+      }
+      plan.tasks.push_back(vt);
+    }
+  }
+  const std::uint32_t acc_end = static_cast<std::uint32_t>(plan.tasks.size());
+  auto split_phase = [&](PhaseKind kind, std::uint32_t t0, std::uint32_t t1) {
+    Phase ph{kind, cur_stage, t0, t1, 0, 0.0, 0.0, 0.0};
+    for (std::uint32_t t = t0; t < t1; ++t) {
+      const Task& tk = plan.tasks[t];
+      for (std::uint32_t sg = tk.seg_begin; sg < tk.seg_end; ++sg) {
+        const double k = plan.tile_src[sg].k, rows = plan.tile_src[sg].m;
+        ph.flops_per_col += 2.0 * rows * k;
+        ph.gen_bytes += 8.0 * rows * k;
+        ph.io_bytes_per_col += 8.0 * k / std::max<std::uint32_t>(1, plan.yp_tiles[tk.node]);
+      }
+      ph.io_bytes_per_col += 8.0 * tk.m * (kind == kPhaseLeaf && tk.id_off != kNoMap ? 2 : 1);
+    }
+    plan.split_phases.push_back(ph);
+  };
+  if (near_end > near_begin) split_phase(kPhaseNear, near_begin, near_end);
+  if (acc_end > near_end) split_phase(kPhaseLeaf, near_end, acc_end);
   if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: too many GEMM segments");
   return true;

@@ -96,7 +96,9 @@ struct Task {
 };
 static_assert(sizeof(Task) == 40, "Task layout");
 
-enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2 };
+// kPhaseNear: Y'_i = sum_j D_ij Wp_j (depends on Wp only); kPhaseLeaf: Y'_i += V_i S_i
+// (accumulates onto the near rows of the same leaf through the task's identity rows).
+enum PhaseKind : int { kPhaseUp = 0, kPhaseDown = 1, kPhaseLeaf = 2, kPhaseNear = 3 };
 
 struct Phase {
   PhaseKind kind;
@@ -123,7 +125,11 @@ struct Plan {
   std::vector<std::uint32_t> chunk_seg; // pre-tiled chunk -> segment
   std::uint64_t tile_elems = 0;
   std::vector<Phase> phases;
+  // the leaf phase as a near phase + an accumulating leaf phase over the same segments
+  // (tasks after the phases' ones); the DAG uses it for narrow column counts
+  std::vector<Phase> split_phases;
   std::vector<std::uint32_t> node_tiles;  // row tiles of each active node's T (= of its S)
+  std::vector<std::uint32_t> yp_tiles;    // near-phase row tiles of each leaf (its Yp rows)
   // subtree-split mode (SURVEY §8e fallback): nodes whose T arrives through the exchange
   std::uint32_t nparts = 1, part = 0;
   std::vector<std::uint32_t> remote_t_nodes;
