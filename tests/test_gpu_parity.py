@@ -195,3 +195,27 @@ def test_dag_launch_equals_level_launches(name, q):
     b = ev.evaluate(w, levels=True)
     assert np.array_equal(a, b)
     assert oracle.rel_frob(a, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+
+
+@pytest.mark.parametrize("q", [1, 7, 63, 65, 129, 257, 320])
+def test_ragged_column_counts(q):
+    """Every column count, narrow (split leaf variant, ≤4 blocks) and wide, partial last
+    blocks included: the oracle's result, and the DAG equal to the level launches."""
+    inst = build_instance(InstanceSpec(n=3000, d=3, leaf=48, max_rank=40, mode="tau", tau=0.7, seed=12))
+    ev = Evaluator(inst.cds)
+    w = _w(inst.cds.n, q, 5)
+    y = ev.evaluate(w)
+    assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    assert np.array_equal(y, ev.evaluate(w, levels=True))
+    ev.close()
+    inst.close()
+
+
+@pytest.mark.parametrize("n,leaf", [(40, 16), (129, 64), (2, 1)])
+def test_tiny_trees(n, leaf):
+    """Two-level and single-point-leaf trees (structure.cpp:35-36 rejects one-node trees)."""
+    inst = build_instance(InstanceSpec(n=n, d=2, leaf=leaf, max_rank=8, seed=3))
+    w = _w(n, 5, 2)
+    y = evaluate(inst.cds, EvalPlan(), w)
+    assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    inst.close()
