@@ -619,7 +619,9 @@ using namespace hmxg;
 extern "C" {
 
 const char* hmxg_last_error(void) { return g_err.c_str(); }
-const char* hmxg_version(void) { return "hmxg 0.3 sm_100a fp64-dmma tma-pipelined grouped-gemm"; }
+const char* hmxg_version(void) {
+  return "hmxg 0.4 sm_100a fp64-dmma tma-pipelined dag; identity-row lowering; generated blocks; gpu id";
+}
 
 int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
   if (!out) return set_err(HMXG_EINVAL, "hmxg_create: null out");
