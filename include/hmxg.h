@@ -102,13 +102,16 @@ typedef struct hmxg_info {
   uint32_t num_devices;
   uint32_t launches_per_eval;         /* kernels per evaluate call per device (3: permute-in,
                                          the whole-evaluation DAG launch, permute-out) */
-  double flops_per_col;               /* 2*(2|V|+|B|+|D|) */
+  double flops_per_col;               /* 2*(2|V|+|B|+|D|), the reference's count */
   uint64_t device_bytes;              /* resident generator + table bytes per device */
+  double exec_flops_per_col;          /* flops the kernels execute per column (the bases'
+                                         identity rows become row copies) */
 } hmxg_info;
 
 /* One launch of the per-evaluation launch sequence (SURVEY §7.3 / DESIGN.md):
  * kind 0 gather, 1 upward (level = subtree height), 2 far+downward (level = depth),
- * 3 near+leaf-downward, 4 scatter, 5 the whole-evaluation DAG launch (every GEMM tile of
+ * 3 near+leaf-downward, 4 scatter, 5 the whole-evaluation DAG launch, 6 near field alone
+ * (the split leaf variant of narrow column counts) (every GEMM tile of
  * every level; the default sequence is gather, DAG, scatter). Byte/flop fields are ALGORITHMIC (each operand block
  * counted once): the roofline numerators of bench.py. last_ms is the device time of that
  * launch in the last evaluation run with HMXG_F_TIME_PHASES on device 0. */

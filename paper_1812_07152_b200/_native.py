@@ -91,6 +91,7 @@ class Info(C.Structure):
         ("launches_per_eval", C.c_uint32),
         ("flops_per_col", C.c_double),
         ("device_bytes", C.c_uint64),
+        ("exec_flops_per_col", C.c_double),
     ]
 
 

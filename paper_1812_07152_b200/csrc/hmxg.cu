@@ -666,6 +666,7 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
     info->skel_rows = plan.skel_rows;
     info->launches_per_eval = 3;
     info->flops_per_col = 2.0 * (2.0 * plan.v_elems + plan.b_elems + plan.d_elems);
+    for (const Phase& ph : plan.phases) info->exec_flops_per_col += ph.flops_per_col;
   }
   return HMXG_OK;
 }
@@ -819,6 +820,7 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   info->num_devices = static_cast<std::uint32_t>(mat->devs.size());
   info->launches_per_eval = 3;  // permute-in, eval_dag, permute-out
   info->flops_per_col = 2.0 * (2.0 * p.v_elems + p.b_elems + p.d_elems);
+  for (const Phase& ph : p.phases) info->exec_flops_per_col += ph.flops_per_col;
   info->device_bytes = mat->devs.empty() ? 0 : mat->devs[0].resident_bytes;
   return HMXG_OK;
 }

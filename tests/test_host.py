@@ -197,3 +197,35 @@ def test_builder_accuracy_tracks_tolerance():
         exact = inst.dense_rows(rows, w)
         errs.append(np.linalg.norm(y[rows] - exact) / np.linalg.norm(exact))
     assert errs[1] < errs[0] and errs[1] < 1e-3
+
+
+def test_identity_rows_lowering_counts():
+    """The plan drops exactly the multiply-adds of the bases' unit rows of internal
+    parents (plan.cpp identity rows): executed flops = reference flops - 2 x (unit-row
+    elements of every internal node's V, once upward and once downward)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1812_07152_b200 import InstanceSpec, build_instance
+    from paper_1812_07152_b200 import _native as N
+
+    inst = build_instance(InstanceSpec(n=6000, d=3, leaf=64, max_rank=48, seed=8))
+    c = inst.cds
+    unit = 0
+    for node in range(c.num_nodes):
+        if c.lchild[node] == N.HMXG_NO_NODE or c.sranks[node] == 0 or not c.participating[node]:
+            continue
+        v = c.extract_v(node)
+        claimed = set()
+        for r in v:  # a unit row claims its column once (plan.cpp)
+            nz = np.flatnonzero(r)
+            if nz.size == 1 and r[nz[0]] == 1.0 and nz[0] not in claimed:
+                claimed.add(nz[0])
+                unit += v.shape[1]
+    info = N.Info()
+    view = c.view()
+    assert N.hmxg().hmxg_validate(C.byref(view), C.byref(info)) == N.HMXG_OK
+    assert unit > 0
+    assert info.exec_flops_per_col == pytest.approx(info.flops_per_col - 2 * 2 * unit, rel=1e-12)
+    inst.close()
