@@ -344,8 +344,8 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.claim = d.dag_done;
     dp.done = d.dag_done + kDagClaimWords;
     dp.node_tiles = d.node_tiles;
-  dp.yp_tiles = d.yp_tiles;
     dp.yp_tiles = d.yp_tiles;
+    dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
     p.tasks = d.tasks;
@@ -752,6 +752,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.done = d.dag_done + kDagClaimWords;
   dp.node_tiles = d.node_tiles;
   dp.yp_tiles = d.yp_tiles;
+  dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
   const dim3 pgrid((nn + kTT - 1) / kTT, (qq + kTT - 1) / kTT);

@@ -536,6 +536,7 @@ struct DagParams {
   const std::uint32_t* node_tiles;
   const std::uint32_t* yp_tiles;  // near-phase row tiles per leaf
   std::uint32_t ncb, nodes;
+  std::uint32_t signal_yp;        // the split leaf variant runs: Yp tiles are waited on
 };
 
 __device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
@@ -619,9 +620,11 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         (void)ld_acquire(ctr);
       }
     });
-    // Yp rows: the leaf phase accumulates onto the near phase's rows of the same leaf
-    warp_signal((task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
-                static_cast<std::uint64_t>(task.node) * d.ncb + cb);
+    // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
+    // phase accumulates onto the near phase's rows of the same leaf)
+    if (task.cbuf != kBufYp || d.signal_yp)
+      warp_signal((task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
+                  static_cast<std::uint64_t>(task.node) * d.ncb + cb);
   }
 }
 
