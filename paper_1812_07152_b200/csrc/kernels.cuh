@@ -402,9 +402,41 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // Identity rows of the bases: the accumulator starts as the exact row copy from T
-  // (upward) or S (downward). The loads are issued before the K loop, so they are in
-  // flight while the first chunks arrive.
+  // The accumulator starts from rows that are already complete: the task's own C rows
+  // (kTaskAccumulate: the leaf phase onto the near phase's rows), plus the identity rows
+  // of the bases, exact row copies from Wp or T (upward) or S (downward). The loads are
+  // issued before the K loop, so they are in flight while the first chunks arrive.
+  // `add` false: the rows are the accumulator's first value (assigned, so no instruction
+  // waits for the loads before the first DMMA needs the accumulator); true: added to it
+  auto add_rows = [&](const double* B, std::uint64_t ldb, const std::uint32_t (&src)[4], bool add) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (src[i] == kNoMap) continue;
+      const double* srow = B + static_cast<std::uint64_t>(src[i]) * ldb + cb * kCbPitch;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = (2 * j + wn) * 8 + 2 * fk;
+        if (col + 1 < static_cast<int>(ncols)) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(srow + col));
+          acc[i][j][0] = add ? acc[i][j][0] + v.x : v.x;
+          acc[i][j][1] = add ? acc[i][j][1] + v.y : v.y;
+        } else if (col < static_cast<int>(ncols)) {
+          const double v = __ldcg(srow + col);
+          acc[i][j][0] = add ? acc[i][j][0] + v : v;
+        }
+      }
+    }
+  };
+  if (task.flags & kTaskAccumulate) {
+    std::uint32_t own[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (2 * i + wm) * 8 + fr;
+      own[i] = row < task.m ? task.c_row + row : kNoMap;
+    }
+    wait_id(task, true);
+    add_rows(pick_buf(p, task.cbuf), pick_ld(p, task.cbuf), own, false);
+  }
   if (task.id_off != kNoMap) {
     std::uint32_t srcs[4];  // static sources: fetched while the producing nodes may still run
 #pragma unroll
@@ -412,26 +444,11 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
       const int row = (2 * i + wm) * 8 + fr;
       srcs[i] = row < task.m ? __ldg(p.idmap + task.id_off + row) : kNoMap;
     }
-    wait_id(task);
-    const double* B = pick_buf(p, task.id_buf);
-    const std::uint64_t ldb = pick_ld(p, task.id_buf);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const std::uint32_t src = srcs[i];
-      if (src == kNoMap) continue;
-      const double* srow = B + static_cast<std::uint64_t>(src) * ldb + cb * kCbPitch;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = (2 * j + wn) * 8 + 2 * fk;
-        if (col + 1 < static_cast<int>(ncols)) {
-          const double2 v = __ldcg(reinterpret_cast<const double2*>(srow + col));
-          acc[i][j][0] = v.x;
-          acc[i][j][1] = v.y;
-        } else if (col < static_cast<int>(ncols)) {
-          acc[i][j][0] = __ldcg(srow + col);
-        }
-      }
-    }
+    wait_id(task, false);
+    if (task.flags & kTaskAccumulate)
+      add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, true);
+    else
+      add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, false);
   }
 
   // Predicated-off DMMAs still occupy the tensor pipe, so ragged tiles branch (warp-
@@ -510,7 +527,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
     const std::uint64_t t = take_item(c, seq);
     if (t >= ntiles) break;
     consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks), fa, it,
-                      [](const Task&) {});  // the copied rows' level ran in an earlier launch
+                      [](const Task&, bool) {});  // the copied rows' level ran in an earlier launch
   }
 }
 
@@ -607,18 +624,24 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
     const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-    consume_gemm_tile(p, c, task, cb, fa, it, [&](const Task& t) {
-      // the nodes whose rows are copied are complete for this column block; every lane
-      // acquires, the copies are plain (L2) loads
-      for (const std::uint32_t node : {t.id_node0, t.id_node1}) {
-        if (node == kNoMap) continue;
-        const std::uint32_t* ctr = (t.id_buf == kBufT ? done_t : (t.id_buf == kBufS ? done_s : done_y)) +
-                                   static_cast<std::uint64_t>(node) * d.ncb + cb;
-        const std::uint32_t tiles = t.id_buf == kBufYp ? d.yp_tiles[node] : d.node_tiles[node];
-        if (lane == 0) spin_until(ctr, tiles * kConsumerWarps);
+    consume_gemm_tile(p, c, task, cb, fa, it, [&](const Task& t, bool own_rows) {
+      // the rows about to be read are complete for this column block (every lane acquires;
+      // the reads are plain L2 loads): the near phase's rows of this leaf, or the nodes
+      // whose rows are copied (Wp is complete before the launch)
+      auto wait_for = [&](const std::uint32_t* ctr, std::uint32_t target) {
+        if (lane == 0) spin_until(ctr, target);
         __syncwarp();
         (void)ld_acquire(ctr);
+      };
+      if (own_rows) {
+        wait_for(done_y + static_cast<std::uint64_t>(t.node) * d.ncb + cb, d.yp_tiles[t.node] * kConsumerWarps);
+        return;
       }
+      if (t.id_buf == kBufWp) return;
+      for (const std::uint32_t node : {t.id_node0, t.id_node1})
+        if (node != kNoMap)
+          wait_for((t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb,
+                   d.node_tiles[node] * kConsumerWarps);
     });
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)

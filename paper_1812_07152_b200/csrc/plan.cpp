@@ -140,11 +140,53 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   }
   if (prow > std::numeric_limits<std::uint32_t>::max() - kRowAlign) return fail(err, "cds: too many points");
   plan.rows_pad = prow;
+  // Leaf point orders (identity rows, below): a leaf basis V_i has a unit row for every
+  // skeleton point, so its points are ordered [points dense in V_i, skeleton points]. The
+  // upward K range is then a prefix of the leaf's Wp rows and the downward V_i product a
+  // prefix of its Y' rows; the skeleton points become row copies.
+  std::vector<std::vector<std::uint32_t>> lpt(nn), lpt_pos(nn);  // new row -> old position; inverse
+  std::vector<std::vector<std::uint32_t>> leaf_unit_col(nn);     // old position -> V column (kNoMap)
+  std::vector<std::vector<std::uint32_t>> leaf_col_src(nn);      // V column -> old position (kNoMap)
+  std::vector<std::uint32_t> dense_pts(nn, 0), pt_map_off(nn, kNoMap);
+  for (std::uint32_t i = 0; i < nn; ++i) dense_pts[i] = size_of(i);
+  if (split.identity_rows && v.num_v) {
+    for (std::uint32_t i : leaves_by_start) {
+      if (!(v.participating[i] && v.sranks[i] > 0)) continue;
+      const std::uint64_t W = size_of(i), K = v.sranks[i];
+      const double* V = v.vgen + v.vptr[vslot[i]];
+      leaf_unit_col[i].assign(W, kNoMap);
+      leaf_col_src[i].assign(K, kNoMap);
+      for (std::uint64_t r = 0; r < W; ++r) {
+        std::uint64_t nz = 0, col = 0;
+        for (std::uint64_t j = 0; j < K && nz < 2; ++j)
+          if (V[r + j * W] != 0.0) {
+            ++nz;
+            col = j;
+          }
+        if (nz != 1 || V[r + col * W] != 1.0 || leaf_col_src[i][col] != kNoMap) continue;
+        leaf_unit_col[i][r] = static_cast<std::uint32_t>(col);
+        leaf_col_src[i][col] = static_cast<std::uint32_t>(r);
+      }
+      for (std::uint32_t r = 0; r < W; ++r)
+        if (leaf_unit_col[i][r] == kNoMap) lpt[i].push_back(r);
+      dense_pts[i] = static_cast<std::uint32_t>(lpt[i].size());
+      if (dense_pts[i] == W) {
+        lpt[i].clear();
+        continue;
+      }
+      for (std::uint32_t r = 0; r < W; ++r)
+        if (leaf_unit_col[i][r] != kNoMap) lpt[i].push_back(r);
+      lpt_pos[i].assign(W, 0);
+      for (std::uint32_t q = 0; q < W; ++q) lpt_pos[i][lpt[i][q]] = q;
+      pt_map_off[i] = static_cast<std::uint32_t>(plan.maps.size());
+      plan.maps.insert(plan.maps.end(), lpt[i].begin(), lpt[i].end());
+    }
+  }
   plan.pmap.assign(prow, 0xffffffffu);
   plan.ipmap.assign(v.n, 0);
   for (std::uint32_t i : leaves_by_start)
     for (std::uint32_t r = 0; r < size_of(i); ++r) {
-      const std::uint32_t orig = v.perm[v.start[i] + r];
+      const std::uint32_t orig = v.perm[v.start[i] + (lpt[i].empty() ? r : lpt[i][r])];
       plan.pmap[plan.leaf_row[i] + r] = orig;
       plan.ipmap[orig] = static_cast<std::uint32_t>(plan.leaf_row[i] + r);
     }
@@ -339,6 +381,14 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         cur_node = i;
         cur_id.clear();
         cur_id_node0 = cur_id_node1 = kNoMap;
+        if (is_leaf(i) && !lpt[i].empty()) {  // T_i(j) += Wp(skeleton point of column j)
+          cur_id.assign(v.sranks[i], kNoMap);
+          for (std::uint32_t r = 0; r < v.sranks[i]; ++r) {
+            const std::uint32_t pos = leaf_col_src[i][oldrow(i, r)];
+            if (pos != kNoMap) cur_id[r] = static_cast<std::uint32_t>(plan.leaf_row[i] + lpt_pos[i][pos]);
+          }
+          cur_id_buf = kBufWp;  // complete before the launch: no wait
+        }
         if (!is_leaf(i) && !colsrc[i].empty()) {  // T_i(j) += T_child(copied row)
           cur_id.assign(v.sranks[i], kNoMap);
           for (std::uint32_t r = 0; r < v.sranks[i]; ++r) {
@@ -353,8 +403,9 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         }
         add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
           // A = V_i^T: tile row r is column oldrow(i, r) of V_i
-          if (is_leaf(i)) {
-            push_seg(kGenV, true, vo, lda, lda, m, kBufWp, plan.leaf_row[i], 0, r0, map_off[i], kNoMap, m);
+          if (is_leaf(i)) {  // K: the leaf's dense points (a prefix of its rows)
+            push_seg(kGenV, true, vo, lda, dense_pts[i], m, kBufWp, plan.leaf_row[i], 0, r0, map_off[i], pt_map_off[i],
+                     m);
           } else {
             const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
             const std::uint64_t srl = v.sranks[lc];
@@ -426,14 +477,22 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     cur_node = i;
     cur_id.clear();
     cur_id_node0 = cur_id_node1 = kNoMap;
+    if (!lpt[i].empty()) {  // Y'_i(skeleton point) += S_i(its column)
+      cur_id.assign(m, kNoMap);
+      for (std::uint32_t r = dense_pts[i]; r < m; ++r)
+        cur_id[r] = static_cast<std::uint32_t>(plan.node_off[i] + newrow(i, leaf_unit_col[i][lpt[i][r]]));
+      cur_id_buf = kBufS;
+      cur_id_node0 = i;
+    }
     const std::uint32_t t0 = static_cast<std::uint32_t>(plan.tasks.size());
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
-      if (active(i))
-        push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, kNoMap, map_off[i],
-                 mt);
+      if (active(i))  // the V_i product covers the dense points (a prefix of the rows)
+        push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, pt_map_off[i],
+                 map_off[i], dense_pts[i] > r0 ? dense_pts[i] - r0 : 0);
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
-        push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, kNoMap, kNoMap, mt);
+        push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, pt_map_off[i],
+                 pt_map_off[j], mt);
       }
     }, plan.phases.back());
     leaf_tasks_of.push_back({i, t0, static_cast<std::uint32_t>(plan.tasks.size())});
@@ -450,7 +509,10 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     plan.yp_tiles[i] = lt.t1 - lt.t0;
     for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
       Task nt = plan.tasks[t];
-      if (with_v) nt.seg_begin += 1;  // drop the V segment (the first of the task)
+      // drop the V segment (the first of the task, when the tile has dense points) and the
+      // skeleton-row copies: both belong to the leaf task below
+      if (nt.seg_end > nt.seg_begin && plan.segs[nt.seg_begin].bbuf == kBufS) nt.seg_begin += 1;
+      nt.id_off = nt.id_node0 = nt.id_node1 = kNoMap;
       plan.tasks.push_back(nt);
     }
   }
@@ -460,13 +522,10 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     if (!active(i)) continue;
     for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
       Task vt = plan.tasks[t];
-      if (split_leaf[i]) {  // V segment only, accumulating onto the near rows of the tile
-        vt.seg_end = vt.seg_begin + 1;
-        vt.id_off = static_cast<std::uint32_t>(plan.idmap.size());
-        for (std::uint32_t r = 0; r < vt.m; ++r) plan.idmap.push_back(vt.c_row + r);
-        vt.id_buf = kBufYp;
-        vt.id_node0 = i;
-        vt.id_node1 = kNoMap;
+      if (split_leaf[i]) {  // V segment (and skeleton copies) accumulated onto the near rows
+        const bool has_v = vt.seg_end > vt.seg_begin && plan.segs[vt.seg_begin].bbuf == kBufS;
+        vt.seg_end = vt.seg_begin + (has_v ? 1 : 0);
+        vt.flags |= kTaskAccumulate;
       }
       plan.tasks.push_back(vt);
     }
@@ -482,7 +541,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         ph.gen_bytes += 8.0 * rows * k;
         ph.io_bytes_per_col += 8.0 * k / std::max<std::uint32_t>(1, plan.yp_tiles[tk.node]);
       }
-      ph.io_bytes_per_col += 8.0 * tk.m * (kind == kPhaseLeaf && tk.id_off != kNoMap ? 2 : 1);
+      ph.io_bytes_per_col += 8.0 * tk.m * (tk.flags & kTaskAccumulate ? 2 : 1);
     }
     plan.split_phases.push_back(ph);
   };

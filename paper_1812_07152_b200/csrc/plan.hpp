@@ -91,10 +91,11 @@ struct Task {
   std::uint32_t id_node0;
   std::uint32_t id_node1;
   std::uint16_t id_buf;
-  std::uint16_t pad0;
+  std::uint16_t flags;  // kTaskAccumulate: the accumulator starts from the task's own C rows
   std::uint32_t pad1;
 };
 static_assert(sizeof(Task) == 40, "Task layout");
+constexpr std::uint16_t kTaskAccumulate = 1;
 
 // kPhaseNear: Y'_i = sum_j D_ij Wp_j (depends on Wp only); kPhaseLeaf: Y'_i += V_i S_i
 // (accumulates onto the near rows of the same leaf through the task's identity rows).

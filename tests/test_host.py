@@ -200,9 +200,9 @@ def test_builder_accuracy_tracks_tolerance():
 
 
 def test_identity_rows_lowering_counts():
-    """The plan drops exactly the multiply-adds of the bases' unit rows of internal
-    parents (plan.cpp identity rows): executed flops = reference flops - 2 x (unit-row
-    elements of every internal node's V, once upward and once downward)."""
+    """The plan drops exactly the multiply-adds of the bases' unit rows (plan.cpp
+    identity rows): executed flops = reference flops - 2 x 2 x (unit-row elements of every
+    active node's V), once upward and once downward."""
     import ctypes as C
 
     import numpy as np
@@ -214,7 +214,7 @@ def test_identity_rows_lowering_counts():
     c = inst.cds
     unit = 0
     for node in range(c.num_nodes):
-        if c.lchild[node] == N.HMXG_NO_NODE or c.sranks[node] == 0 or not c.participating[node]:
+        if c.sranks[node] == 0 or not c.participating[node]:
             continue
         v = c.extract_v(node)
         claimed = set()
