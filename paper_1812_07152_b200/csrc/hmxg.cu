@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -295,6 +297,56 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   return HMXG_OK;
 }
 
+#ifdef HMXG_TRACE
+// Diagnostic builds only (tools/dag_trace.py): per-item globaltimer stamps of the last
+// eval_dag launch, written as CSV to $HMXG_TRACE_OUT after a synchronous evaluation.
+unsigned long long* g_trace = nullptr;
+std::size_t g_trace_words = 0;
+int trace_prepare(const DevState& d, cudaStream_t st) {
+  const std::size_t words = std::size_t(d.gemm_grid) * kTraceSeq * kTraceWords;
+  if (words > g_trace_words) {
+    cudaFree(g_trace);
+    HMXG_CUDA(cudaMalloc(&g_trace, words * sizeof(unsigned long long)));
+    g_trace_words = words;
+  }
+  HMXG_CUDA(cudaMemsetAsync(g_trace, 0, words * sizeof(unsigned long long), st));
+  return HMXG_OK;
+}
+void trace_dump(const Plan& plan, std::size_t q) {
+  const char* path = std::getenv("HMXG_TRACE_OUT");
+  if (!path || !g_trace) return;
+  std::vector<unsigned long long> h(g_trace_words);
+  if (cudaMemcpy(h.data(), g_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0);
+  std::vector<const Phase*> phs;
+  for (const Phase& ph : plan.phases) phs.push_back(&ph);
+  for (const Phase& ph : plan.split_phases) phs.push_back(&ph);
+  FILE* f = std::fopen(path, "w");
+  if (!f) return;
+  std::fprintf(f, "cta,seq,sm,item,task,cb,kind,level,m,segs,t_claim,t_issued,t_take,t_kend,t_done\n");
+  for (std::size_t b = 0; b < g_trace_words / (kTraceSeq * kTraceWords); ++b)
+    for (int s = 0; s < kTraceSeq; ++s) {
+      const unsigned long long* r = &h[(b * kTraceSeq + s) * kTraceWords];
+      if (r[1] == 0) continue;
+      const std::uint32_t qi = static_cast<std::uint32_t>(r[0]);
+      if (qi >= items.size()) continue;
+      const std::uint32_t task = static_cast<std::uint32_t>(items[qi]);
+      const std::uint32_t cb = static_cast<std::uint32_t>(items[qi] >> 32) & 0xffffffu;
+      int kind = -1, level = -1;
+      for (const Phase* ph : phs)
+        if (task >= ph->task_begin && task < ph->task_end) {
+          kind = ph->kind;
+          level = static_cast<int>(ph->level);
+        }
+      const Task& tk = plan.tasks[task];
+      std::fprintf(f, "%zu,%d,%llu,%u,%u,%u,%d,%d,%u,%u,%llu,%llu,%llu,%llu,%llu\n", b, s, r[0] >> 32, qi, task, cb,
+                   kind, level, tk.m, tk.seg_end - tk.seg_begin, r[1], r[2], r[3], r[4], r[5]);
+    }
+  std::fclose(f);
+}
+#endif
+
 // Default: one whole-evaluation DAG launch. `levels`: the level-by-level launch sequence
 // (permute-in, one launch per tree level, permute-out) for per-launch breakdowns.
 int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw, double* y,
@@ -349,6 +401,10 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
     p.tasks = d.tasks;
+#ifdef HMXG_TRACE
+    HMXG_TRY(trace_prepare(d, st));
+    dp.trace = g_trace;
+#endif
     HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
     HMXG_TRY(mark());
     const dim3 pgrid2((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
@@ -755,6 +811,10 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
+#ifdef HMXG_TRACE
+  HMXG_TRY(trace_prepare(d, st));
+  dp.trace = g_trace;
+#endif
   const dim3 pgrid((nn + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
   if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_split_stage: too many columns for one call");
   if (stage == 0) {
@@ -934,6 +994,9 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       HMXG_CUDA(cudaEventRecord(d.ev1, st));
       HMXG_CUDA(cudaEventSynchronize(d.ev1));
       HMXG_CUDA(cudaEventElapsedTime(&dev_ms, d.ev0, d.ev1));
+#ifdef HMXG_TRACE
+      if (!levels) trace_dump(plan, q);
+#endif
     }
   } else {
     // column sharding over the context's devices: Y[:,c] depends only on W[:,c]

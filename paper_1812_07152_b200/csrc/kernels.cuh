@@ -384,10 +384,13 @@ __device__ __forceinline__ FragAddr frag_addresses(int wm, int wn, int fr, int f
 // Consumers: the K loop and epilogue of one GEMM tile (each element stored exactly once).
 // `wait_id(task)` runs before the identity rows are read (the DAG kernel's wait for the
 // nodes that produce them; a no-op per level, where they ran in an earlier launch).
-template <class WaitId>
+struct NoHook {
+  __device__ void operator()() const {}
+};
+template <class WaitId, class KEnd = NoHook>
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
                                                   std::uint32_t cb, const FragAddr& fa, std::uint32_t& it,
-                                                  WaitId&& wait_id) {
+                                                  WaitId&& wait_id, KEnd&& k_end = KEnd{}) {
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
@@ -437,14 +440,21 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     wait_id(task, true);
     add_rows(pick_buf(p, task.cbuf), pick_ld(p, task.cbuf), own, false);
   }
-  if (task.id_off != kNoMap) {
-    std::uint32_t srcs[4];  // static sources: fetched while the producing nodes may still run
+  // Identity sources are static: fetched while the producing nodes may still run. Leaf
+  // tasks (kTaskIdLast) add the copied rows after the K loop, so that the combined and the
+  // split leaf variants sum in one order; the other tasks start the accumulator with them.
+  const bool has_id = task.id_off != kNoMap;
+  const bool id_last = (task.flags & kTaskIdLast) != 0;
+  std::uint32_t srcs[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = (2 * i + wm) * 8 + fr;
-      srcs[i] = row < task.m ? __ldg(p.idmap + task.id_off + row) : kNoMap;
-    }
+  for (int i = 0; i < 4; ++i) {
+    const int row = (2 * i + wm) * 8 + fr;
+    srcs[i] = has_id && row < task.m ? __ldg(p.idmap + task.id_off + row) : kNoMap;
+  }
+  if (has_id && !id_last) {
     wait_id(task, false);
+    // `add` must stay a compile-time constant: a runtime select would wait for the loads
+    // here, before the K loop, instead of at the first DMMA
     if (task.flags & kTaskAccumulate)
       add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, true);
     else
@@ -471,6 +481,11 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     } else {
       consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nch, it, live_i, live_j);
     }
+  }
+  k_end();
+  if (has_id && id_last) {
+    if (!(task.flags & kTaskIdSynced)) wait_id(task, false);
+    add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, true);
   }
 
   double* C = pick_buf(p, task.cbuf);
@@ -554,7 +569,41 @@ struct DagParams {
   const std::uint32_t* yp_tiles;  // near-phase row tiles per leaf
   std::uint32_t ncb, nodes;
   std::uint32_t signal_yp;        // the split leaf variant runs: Yp tiles are waited on
+#ifdef HMXG_TRACE
+  // diagnostic builds (tools/dag_trace.py): per claimed item, kTraceWords globaltimer stamps
+  unsigned long long* trace;
+#endif
 };
+#ifdef HMXG_TRACE
+// per (CTA, claim sequence): smid << 32 | item index, claim, producer issued the item's last
+// chunk, consumer warp 0 took the item, its K loop ended, its tile was stored and signalled
+constexpr int kTraceWords = 6;
+constexpr int kTraceSeq = 4096;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+template <class D>
+__device__ __forceinline__ unsigned long long* trace_slot(const D& d, std::uint32_t seq) {
+  return seq < kTraceSeq ? d.trace + (static_cast<std::uint64_t>(blockIdx.x) * kTraceSeq + seq) * kTraceWords
+                         : nullptr;
+}
+#define HMXG_STAMP(seq, k) \
+  do {                                                                    \
+    unsigned long long* tr_ = trace_slot(d, seq);                         \
+    if (tr_) tr_[k] = gtimer();                                           \
+  } while (0)
+#else
+#define HMXG_STAMP(seq, k) \
+  do {                     \
+  } while (0)
+#endif
 
 __device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
   std::uint32_t v;
@@ -601,6 +650,13 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t q = atomicAdd(d.claim, 1u);
         const std::uint64_t item = q < d.nitems ? d.items[q] : make_item(kItemEnd, 0, 0);
+#ifdef HMXG_TRACE
+        unsigned long long* tr = trace_slot(d, seq);
+        if (tr && q < d.nitems) {
+          tr[0] = (static_cast<unsigned long long>(smid()) << 32) | q;
+          tr[1] = gtimer();
+        }
+#endif
         post_item(c, seq, item);
         if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
         const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
@@ -612,6 +668,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
           // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
         });
+        HMXG_STAMP(seq, 2);
       }
     }
     return;
@@ -622,6 +679,8 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   for (std::uint32_t seq = 0;; ++seq) {
     const std::uint64_t item = take_item(c, seq);
     if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
+    const bool stamp = threadIdx.x == 0;
+    if (stamp) HMXG_STAMP(seq, 3);
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
     const Task task = p.tasks[static_cast<std::uint32_t>(item)];
     consume_gemm_tile(p, c, task, cb, fa, it, [&](const Task& t, bool own_rows) {
@@ -642,12 +701,15 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         if (node != kNoMap)
           wait_for((t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb,
                    d.node_tiles[node] * kConsumerWarps);
+    }, [&]() {
+      if (stamp) HMXG_STAMP(seq, 4);
     });
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
     if (task.cbuf != kBufYp || d.signal_yp)
       warp_signal((task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
                   static_cast<std::uint64_t>(task.node) * d.ncb + cb);
+    if (stamp) HMXG_STAMP(seq, 5);
   }
 }
 

@@ -459,17 +459,20 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     close_phase();
   }
 
-  // --- leaves: Y'_i = V_i S_i + sum_{near (i,j)} D_ij Wp_j, one task per leaf row tile
-  //     (kPhaseLeaf, every leaf row written once; the V segment first, then the D ones).
+  // --- leaves: Y'_i = sum_{near (i,j)} D_ij Wp_j + V_i S_i, one task per leaf row tile
+  //     (kPhaseLeaf, every leaf row written once; the D segments first, then the V one,
+  //     then the skeleton points' copied S_i rows, kTaskIdLast).
   //     The split variant (Plan::split_phases) runs the same D segments as a near task that
-  //     needs only Wp, and the V segment as a leaf task that accumulates onto the near rows
-  //     (identity rows from Yp): the DAG can then fill the tree passes' idle slots with
-  //     near-field tiles. Both variants share the segments and pre-tiled operands.
+  //     needs only Wp, and the V segment as a leaf task that accumulates onto the near rows:
+  //     the DAG can then fill the tree passes' idle slots with near-field tiles. Both
+  //     variants share the segments and pre-tiled operands and sum in the same order, so
+  //     they give the same bits (every column of Y is independent of how Q is split).
   plan.yp_tiles.assign(nn, 0);
   struct LeafTasks {
     std::uint32_t node, t0, t1;  // combined tasks [t0, t1) in plan.tasks
   };
   std::vector<LeafTasks> leaf_tasks_of;
+  const std::uint32_t lt0_all = static_cast<std::uint32_t>(plan.tasks.size());
   open_phase(kPhaseLeaf, 0);
   for (std::uint32_t i : order) {
     if (!is_leaf(i) || !mine(i)) continue;
@@ -486,19 +489,21 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     }
     const std::uint32_t t0 = static_cast<std::uint32_t>(plan.tasks.size());
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
-      if (active(i))  // the V_i product covers the dense points (a prefix of the rows)
-        push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, pt_map_off[i],
-                 map_off[i], dense_pts[i] > r0 ? dense_pts[i] - r0 : 0);
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
         push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, pt_map_off[i],
                  pt_map_off[j], mt);
       }
+      if (active(i))  // the V_i product covers the dense points (a prefix of the rows)
+        push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, pt_map_off[i],
+                 map_off[i], dense_pts[i] > r0 ? dense_pts[i] - r0 : 0);
     }, plan.phases.back());
+    for (std::uint32_t t = t0; t < plan.tasks.size(); ++t) plan.tasks[t].flags |= kTaskIdLast;
     leaf_tasks_of.push_back({i, t0, static_cast<std::uint32_t>(plan.tasks.size())});
   }
   close_phase();
   // split variant: near tasks, then leaf tasks accumulating onto them
+  auto has_v_seg = [&](const Task& t) { return t.seg_end > t.seg_begin && plan.segs[t.seg_end - 1].bbuf == kBufS; };
   const std::uint32_t near_begin = static_cast<std::uint32_t>(plan.tasks.size());
   std::vector<std::uint8_t> split_leaf(nn, 0);
   for (const LeafTasks& lt : leaf_tasks_of) {
@@ -509,10 +514,11 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     plan.yp_tiles[i] = lt.t1 - lt.t0;
     for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
       Task nt = plan.tasks[t];
-      // drop the V segment (the first of the task, when the tile has dense points) and the
+      // drop the V segment (the last of the task, when the tile has dense points) and the
       // skeleton-row copies: both belong to the leaf task below
-      if (nt.seg_end > nt.seg_begin && plan.segs[nt.seg_begin].bbuf == kBufS) nt.seg_begin += 1;
+      if (has_v_seg(nt)) nt.seg_end -= 1;
       nt.id_off = nt.id_node0 = nt.id_node1 = kNoMap;
+      nt.flags = 0;
       plan.tasks.push_back(nt);
     }
   }
@@ -523,14 +529,19 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     for (std::uint32_t t = lt.t0; t < lt.t1; ++t) {
       Task vt = plan.tasks[t];
       if (split_leaf[i]) {  // V segment (and skeleton copies) accumulated onto the near rows
-        const bool has_v = vt.seg_end > vt.seg_begin && plan.segs[vt.seg_begin].bbuf == kBufS;
-        vt.seg_end = vt.seg_begin + (has_v ? 1 : 0);
+        vt.seg_begin = has_v_seg(vt) ? vt.seg_end - 1 : vt.seg_end;
         vt.flags |= kTaskAccumulate;
       }
       plan.tasks.push_back(vt);
     }
   }
   const std::uint32_t acc_end = static_cast<std::uint32_t>(plan.tasks.size());
+  for (std::uint32_t t = lt0_all; t < acc_end; ++t) {
+    Task& tk = plan.tasks[t];
+    if ((tk.flags & kTaskIdLast) && tk.id_off != kNoMap && tk.id_node1 == kNoMap && has_v_seg(tk) &&
+        plan.segs[tk.seg_end - 1].src == tk.id_node0)
+      tk.flags |= kTaskIdSynced;
+  }
   auto split_phase = [&](PhaseKind kind, std::uint32_t t0, std::uint32_t t1) {
     Phase ph{kind, cur_stage, t0, t1, 0, 0.0, 0.0, 0.0};
     for (std::uint32_t t = t0; t < t1; ++t) {

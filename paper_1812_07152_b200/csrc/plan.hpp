@@ -91,11 +91,20 @@ struct Task {
   std::uint32_t id_node0;
   std::uint32_t id_node1;
   std::uint16_t id_buf;
-  std::uint16_t flags;  // kTaskAccumulate: the accumulator starts from the task's own C rows
+  std::uint16_t flags;  // kTaskAccumulate, kTaskIdLast
   std::uint32_t pad1;
 };
 static_assert(sizeof(Task) == 40, "Task layout");
+// The accumulator starts from the task's own C rows (the split leaf variant's leaf task).
 constexpr std::uint16_t kTaskAccumulate = 1;
+// The identity rows are added after the K loop instead of starting the accumulator. Leaf
+// (Yp) tasks use it so that both leaf variants sum every row in one order,
+// ((sum_j D_ij Wp_j) + V_i S_i) + copied S_i rows, and give the same bits.
+constexpr std::uint16_t kTaskIdLast = 2;
+// The task's last segment reads the rows of the identity source node (S_i of a leaf): the
+// producer acquired that node's completion before streaming it, and the stage barriers
+// (arrive: release, wait: acquire) carry it to the consumers, which skip their own poll.
+constexpr std::uint16_t kTaskIdSynced = 4;
 
 // kPhaseNear: Y'_i = sum_j D_ij Wp_j (depends on Wp only); kPhaseLeaf: Y'_i += V_i S_i
 // (accumulates onto the near rows of the same leaf through the task's identity rows).

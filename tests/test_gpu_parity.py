@@ -136,6 +136,28 @@ def test_device_pointer_path():
     assert np.array_equal(y, ev.evaluate(w))
 
 
+@pytest.mark.parametrize("name", ["cfg2-h2b", "cfg1-hss"])
+def test_leaf_variants_give_the_same_bits(name):
+    """Wide Q on the device runs the combined leaf tasks; the host path evaluates 64-column
+    chunks, which run the split leaf variant (near tasks, then V_i S_i accumulated). Both
+    sum every row in one order, so the results are equal bit for bit."""
+    import torch
+
+    spec, _ = config(name)
+    inst = build_instance(spec)
+    n, q = inst.cds.n, 320  # 5 column blocks: combined leaf tasks on the device path
+    ev = Evaluator(inst.cds)
+    w = _w(n, q, 8)
+    wd = torch.from_numpy(w.T.copy()).cuda()
+    yd = torch.empty_like(wd)
+    ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, stream=torch_stream())
+    torch.cuda.synchronize()
+    y_dev = yd.cpu().numpy().T
+    assert np.array_equal(y_dev, ev.evaluate(w))
+    assert np.array_equal(y_dev, ev.evaluate(w, levels=True))
+    assert oracle.rel_frob(y_dev, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+
+
 def test_graph_replay_matches_direct_launches():
     import torch
 

@@ -1,0 +1,65 @@
+"""Per-item timeline of one eval_dag launch (dev tool; needs a -DHMXG_TRACE build:
+`bash tools/exp_build.sh -DHMXG_TRACE`). Writes the raw CSV to gpurun_out/trace_<cfg>.csv and
+prints, per phase (kind, level), the item count, when its first item was claimed and its
+last one stored (us from the launch's first claim), and the mean item stages:
+claim->take (ring / producer wait), take->K-loop end, K-loop end->stored (epilogue)."""
+import csv
+import os
+import sys
+from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1812_07152_b200 import Evaluator, build_instance, config  # noqa: E402
+
+KIND = {0: "up", 1: "down", 2: "leaf", 3: "near"}
+
+
+def trace(name: str, q: int | None = None) -> str:
+    spec, q0 = config(name)
+    q = q or q0
+    inst = build_instance(spec)
+    ev = Evaluator(inst.cds)
+    w = torch.randn(q, inst.cds.n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(w)
+    s = torch.cuda.Stream()
+    out = os.path.join("gpurun_out", f"trace_{name}_q{q}.csv")
+    for k in range(4):
+        if k == 3:
+            os.environ["HMXG_TRACE_OUT"] = out
+        ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=s.cuda_stream, sync=True, graph=False)
+    os.environ.pop("HMXG_TRACE_OUT", None)
+    ev.close()
+    inst.close()
+    return out
+
+
+def summarize(path: str) -> None:
+    rows = list(csv.DictReader(open(path)))
+    for r in rows:
+        for k in ("t_claim", "t_issued", "t_take", "t_kend", "t_done"):
+            r[k] = int(r[k])
+    t0 = min(r["t_claim"] for r in rows)
+    t1 = max(r["t_done"] for r in rows)
+    print(f"{path}: {len(rows)} items, launch span {(t1 - t0) / 1e3:.1f} us")
+    ph = defaultdict(list)
+    for r in rows:
+        ph[(int(r["kind"]), int(r["level"]))].append(r)
+    order = sorted(ph, key=lambda k: min(r["t_claim"] for r in ph[k]))
+    print(f"{'phase':>9} {'items':>6} {'first':>8} {'last':>8} {'claim>take':>10} {'take>kend':>10} {'kend>done':>10}")
+    for k in order:
+        rs = ph[k]
+        n = len(rs)
+        first = (min(r["t_claim"] for r in rs) - t0) / 1e3
+        last = (max(r["t_done"] for r in rs) - t0) / 1e3
+        ct = sum(r["t_take"] - r["t_claim"] for r in rs) / n / 1e3
+        tk = sum(r["t_kend"] - r["t_take"] for r in rs) / n / 1e3
+        kd = sum(r["t_done"] - r["t_kend"] for r in rs) / n / 1e3
+        print(f"{KIND.get(k[0], k[0]):>6} L{k[1]:<2} {n:>6} {first:8.2f} {last:8.2f} {ct:10.2f} {tk:10.2f} {kd:10.2f}")
+
+
+if __name__ == "__main__":
+    for arg in sys.argv[1:] or ["cfg1-hss"]:
+        name, _, qs = arg.partition(":")
+        summarize(trace(name, int(qs) if qs else None))
