@@ -216,36 +216,54 @@ constexpr std::uint32_t kAStepBytes = 4 * kBM * 8;       // 4 k rows of the A ch
 constexpr std::uint32_t kBStepBytes = 4 * kBPitch * 8;   // 4 k rows of the B tile
 constexpr std::uint32_t kFragStride = 16 * 8;            // fragments 2i+wm are 16 rows / columns apart
 
-// One tile's K loop for a consumer warp: LI x LJ live 8 x 8 fragments (compile time).
+// One segment's K loop for a consumer warp: LI x LJ live 8 x 8 fragments (compile time).
 // Fragments of k step ks+1 are loaded while step ks multiplies (register double buffer).
+// `last_ks`: live k steps of the last chunk (SegDev::last_ksteps, 0 = all four). The
+// zero-padded tail of a segment's last chunk is not multiplied: that chunk runs a rolled
+// loop over its live k steps (a branch; predicated-off DMMAs would still occupy the pipe).
 template <int LI, int LJ>
 __device__ __forceinline__ void consume_chunks(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
                                                std::uint32_t smem_base, std::uint32_t a_base, std::uint32_t b_base,
-                                               std::uint32_t nchunks, std::uint32_t& it) {
+                                               std::uint32_t nchunks, int last_ks, std::uint32_t& it) {
   for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
     const int stage = it % kStages;
     mbar_wait(&full[stage], (it / kStages) & 1);
     const std::uint32_t sa = smem_base + stage * kStageBytes + a_base;
     const std::uint32_t sb = smem_base + stage * kStageBytes + b_base;
     if (LI > 0 && LJ > 0) {
-      double af[2][4], bf[2][4];
+      if (last_ks == 0 || c + 1 < nchunks) {
+        double af[2][4], bf[2][4];
 #pragma unroll
-      for (int i = 0; i < LI; ++i) af[0][i] = lds64(sa + i * kFragStride);
+        for (int i = 0; i < LI; ++i) af[0][i] = lds64(sa + i * kFragStride);
 #pragma unroll
-      for (int j = 0; j < LJ; ++j) bf[0][j] = lds64(sb + j * kFragStride);
+        for (int j = 0; j < LJ; ++j) bf[0][j] = lds64(sb + j * kFragStride);
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int cur = ks & 1;
-        if (ks + 1 < 4) {
+        for (int ks = 0; ks < 4; ++ks) {
+          const int cur = ks & 1;
+          if (ks + 1 < 4) {
 #pragma unroll
-          for (int i = 0; i < LI; ++i) af[cur ^ 1][i] = lds64(sa + (ks + 1) * kAStepBytes + i * kFragStride);
+            for (int i = 0; i < LI; ++i) af[cur ^ 1][i] = lds64(sa + (ks + 1) * kAStepBytes + i * kFragStride);
 #pragma unroll
-          for (int j = 0; j < LJ; ++j) bf[cur ^ 1][j] = lds64(sb + (ks + 1) * kBStepBytes + j * kFragStride);
+            for (int j = 0; j < LJ; ++j) bf[cur ^ 1][j] = lds64(sb + (ks + 1) * kBStepBytes + j * kFragStride);
+          }
+#pragma unroll
+          for (int i = 0; i < LI; ++i)
+#pragma unroll
+            for (int j = 0; j < LJ; ++j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
         }
+      } else {
+#pragma unroll 1
+        for (int ks = 0; ks < last_ks; ++ks) {
+          double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < LI; ++i)
+          for (int i = 0; i < LI; ++i) af[i] = lds64(sa + ks * kAStepBytes + i * kFragStride);
 #pragma unroll
-          for (int j = 0; j < LJ; ++j) dmma884(acc[i][j], af[cur][i], bf[cur][j]);
+          for (int j = 0; j < LJ; ++j) bf[j] = lds64(sb + ks * kBStepBytes + j * kFragStride);
+#pragma unroll
+          for (int i = 0; i < LI; ++i)
+#pragma unroll
+            for (int j = 0; j < LJ; ++j) dmma884(acc[i][j], af[i], bf[j]);
+        }
       }
     }
     release_stage(&empty[stage]);  // every consumer thread releases the stage after its last read
@@ -255,15 +273,17 @@ __device__ __forceinline__ void consume_chunks(double (&acc)[4][4][2], std::uint
 // Partial column block (Q not a multiple of 64): runtime-predicated fragments.
 __device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std::uint64_t* full, std::uint64_t* empty,
                                                     std::uint32_t smem_base, std::uint32_t a_base,
-                                                    std::uint32_t b_base, std::uint32_t nchunks, std::uint32_t& it,
-                                                    int live_i, int live_j) {
+                                                    std::uint32_t b_base, std::uint32_t nchunks, int last_ks,
+                                                    std::uint32_t& it, int live_i, int live_j) {
   for (std::uint32_t c = 0; c < nchunks; ++c, ++it) {
     const int stage = it % kStages;
     mbar_wait(&full[stage], (it / kStages) & 1);
     const std::uint32_t sa = smem_base + stage * kStageBytes + a_base;
     const std::uint32_t sb = smem_base + stage * kStageBytes + b_base;
+    const int nks = (last_ks == 0 || c + 1 < nchunks) ? 4 : last_ks;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
+      if (ks >= nks) break;
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = i < live_i ? lds64(sa + ks * kAStepBytes + i * kFragStride) : 0.0;
@@ -470,16 +490,17 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     const int rows = sg.rows ? static_cast<int>(sg.rows) : static_cast<int>(task.m);
     const int live_i = min(4, max(0, ((rows + 7) / 8 - wm + 1) / 2));
     const std::uint32_t nch = sg.nchunks;
+    const int lks = sg.last_ksteps;
     if (live_j == 4) {
       switch (live_i) {
-        case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
-        case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
-        case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
-        case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
-        default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nch, it); break;
+        case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
       }
     } else {
-      consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nch, it, live_i, live_j);
+      consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it, live_i, live_j);
     }
   }
   k_end();

@@ -269,8 +269,10 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     ts.rmap = rmap;
     ts.kmap = kmap;
     for (std::uint64_t c = 0; c < chunks; ++c) plan.chunk_seg.push_back(static_cast<std::uint32_t>(plan.segs.size()));
+    const std::uint64_t k_last = k - (chunks - 1) * kRowAlign;  // 1 .. 16
     plan.segs.push_back(SegDev{plan.tile_elems, static_cast<std::uint32_t>(b_row), static_cast<std::uint16_t>(chunks),
-                               static_cast<std::uint16_t>(bbuf), src, rows < m ? rows : 0});
+                               static_cast<std::uint8_t>(bbuf), static_cast<std::uint8_t>(k_last == kRowAlign ? 0 : (k_last + 3) / 4),
+                               src, rows < m ? rows : 0});
     plan.tile_src.push_back(ts);
     plan.tile_elems += chunks * kRowAlign * bm;
   };

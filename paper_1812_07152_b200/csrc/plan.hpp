@@ -60,7 +60,9 @@ struct TileSrc {
 static_assert(sizeof(TileSrc) == 48, "TileSrc layout");
 
 // One K segment of a task as the GEMM kernel sees it: nchunks pre-tiled A chunks at
-// tile_off, and B rows [b_row, b_row + 16*nchunks) of buffer bbuf.
+// tile_off, and B rows [b_row, b_row + 16*nchunks) of buffer bbuf. `last_ksteps`: the
+// last chunk's K rows that carry data, in 4-row DMMA k-steps (0: all four); the rest of
+// it is zero padding the consumers do not multiply.
 // `src` is the node whose T or S rows the segment reads (the DAG kernel waits for that
 // node's tiles of the same column block); unused for Wp. `rows`: the segment only
 // contributes to the tile's first `rows` output rows (its A operand is zero below), so
@@ -69,7 +71,8 @@ struct SegDev {
   std::uint64_t tile_off;
   std::uint32_t b_row;
   std::uint16_t nchunks;
-  std::uint16_t bbuf;
+  std::uint8_t bbuf;
+  std::uint8_t last_ksteps;
   std::uint32_t src;
   std::uint32_t rows;
 };
