@@ -260,6 +260,11 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
   return items;
 }
 
+// eval_dag's producer lanes publish the stored tiles when every CTA runs many items
+// (cfg5-HSS, 660 per CTA: DAG -1.4%); with few (cfg2, 32 per CTA) the producer is the busier
+// side and the consumers release their own tiles (forwarding cost cfg2 +21%).
+std::uint32_t forward_signals(std::uint32_t nitems, unsigned grid) { return nitems >= 128ull * grid ? 1u : 0u; }
+
 // [claim counter per stage | T counters | S counters | Yp counters] (nodes x ncb each)
 constexpr std::size_t kDagClaimWords = 2;
 std::size_t dag_done_words(const Plan& plan, std::size_t q) {
@@ -400,6 +405,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
+    dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);
     p.tasks = d.tasks;
 #ifdef HMXG_TRACE
     HMXG_TRY(trace_prepare(d, st));
@@ -811,6 +817,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
+  dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);
 #ifdef HMXG_TRACE
   HMXG_TRY(trace_prepare(d, st));
   dp.trace = g_trace;

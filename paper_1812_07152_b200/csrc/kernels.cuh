@@ -104,6 +104,44 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
     if (++polls > (1u << 26)) __trap();
   }
 }
+// Non-blocking phase test (acquire at CTA scope when it succeeds).
+__device__ __forceinline__ bool mbar_test(std::uint64_t* bar, unsigned parity) {
+  std::uint32_t done;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+// The producer lane's waits: a short suspended try, then `svc()` (it forwards the
+// consumers' tile signals, eval_dag), so that a producer blocked on its own CTA's
+// consumers still publishes what they finished.
+template <class Svc>
+__device__ __forceinline__ void mbar_wait_svc(std::uint64_t* bar, unsigned parity, Svc&& svc) {
+  std::uint32_t done = 0, polls = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(200u)
+        : "memory");
+    if (done) return;
+    svc();
+    if (++polls > (1u << 26)) __trap();
+  }
+}
+struct NoSvc {
+  __device__ void operator()() const {}
+};
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -303,7 +341,12 @@ __device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std:
 // Shared-memory carve-up of one CTA (both GEMM kernels): kStages x {A chunk, B tile}, the
 // stage barriers, a kTileRing-deep ring of claimed work items and their barriers.
 constexpr int kTileRing = 4;
-constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * 8 + 1024;
+// eval_dag: stored tiles travel from the consumer warps to the producer lane, which
+// publishes them at gpu scope (kSigRing-deep ring: counter address, 0 = nothing, kSigEnd)
+constexpr int kSigRing = 8;
+constexpr std::uint64_t kSigEnd = ~std::uint64_t(0);
+constexpr int kSmemBytes =
+    kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * 8 + 3 * kSigRing * 8 + 1024;
 
 struct CtaSmem {
   unsigned char* stage;    // kStages * kStageBytes, 1024-byte aligned
@@ -312,6 +355,9 @@ struct CtaSmem {
   std::uint64_t* tfull;    // [kTileRing]
   std::uint64_t* tempty;   // [kTileRing]
   std::uint64_t* tring;    // [kTileRing] claimed work items
+  std::uint64_t* sfull;    // [kSigRing] one arrive per consumer warp
+  std::uint64_t* sempty;   // [kSigRing] the producer took the record
+  std::uint64_t* saddr;    // [kSigRing]
 };
 
 __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
@@ -323,6 +369,9 @@ __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
   c.tfull = c.empty + kStages;
   c.tempty = c.tfull + kTileRing;
   c.tring = c.tempty + kTileRing;
+  c.sfull = c.tring + kTileRing;
+  c.sempty = c.sfull + kSigRing;
+  c.saddr = c.sempty + kSigRing;
   return c;
 }
 
@@ -336,15 +385,20 @@ __device__ __forceinline__ void init_barriers(const CtaSmem& c) {
       mbar_init(&c.tfull[s], 1);
       mbar_init(&c.tempty[s], kConsumerWarps * 32);
     }
+    for (int s = 0; s < kSigRing; ++s) {
+      mbar_init(&c.sfull[s], kConsumerWarps);
+      mbar_init(&c.sempty[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 }
 
 // Producer lane: post a claimed work item to the ring (waits for the slot to be free).
-__device__ __forceinline__ void post_item(const CtaSmem& c, std::uint32_t seq, std::uint64_t item) {
+template <class Svc = NoSvc>
+__device__ __forceinline__ void post_item(const CtaSmem& c, std::uint32_t seq, std::uint64_t item, Svc&& svc = Svc{}) {
   const int slot = seq % kTileRing;
-  if (seq >= kTileRing) mbar_wait(&c.tempty[slot], ((seq / kTileRing) - 1) & 1);
+  if (seq >= kTileRing) mbar_wait_svc(&c.tempty[slot], ((seq / kTileRing) - 1) & 1, svc);
   c.tring[slot] = item;
   mbar_arrive(&c.tfull[slot]);  // release: consumers read tring[slot] after their wait
 }
@@ -361,10 +415,11 @@ __device__ __forceinline__ std::uint64_t take_item(const CtaSmem& c, std::uint32
 // Producer lane: stream the A chunks and B tiles of one GEMM tile (column block cb).
 // `wait_dep(seg)` runs before a segment's first load (the DAG kernel's dependency wait; a
 // no-op per level).
-template <class WaitDep>
+template <class WaitDep, class Svc = NoSvc>
 __device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
                                                   std::uint32_t cb, const CUtensorMap* tm_wp, const CUtensorMap* tm_t,
-                                                  const CUtensorMap* tm_s, std::uint32_t& it, WaitDep&& wait_dep) {
+                                                  const CUtensorMap* tm_s, std::uint32_t& it, WaitDep&& wait_dep,
+                                                  Svc&& svc = Svc{}) {
   const int x = static_cast<int>(cb * kCbPitch);
   for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
     const SegDev sg = p.segs[si];
@@ -372,7 +427,7 @@ __device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const Cta
     const CUtensorMap* map = sg.bbuf == kBufWp ? tm_wp : (sg.bbuf == kBufT ? tm_t : tm_s);
     for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
       const int stage = it % kStages;
-      if (it >= kStages) mbar_wait(&c.empty[stage], ((it / kStages) - 1) & 1);
+      if (it >= kStages) mbar_wait_svc(&c.empty[stage], ((it / kStages) - 1) & 1, svc);
       unsigned char* st = c.stage + stage * kStageBytes;
       mbar_expect_tx(&c.full[stage], kChunkBytes + kBTileBytes);
       bulk_g2s(st, p.tiles + sg.tile_off + static_cast<std::uint64_t>(ch) * kChunkElems, kChunkBytes,
@@ -590,6 +645,7 @@ struct DagParams {
   const std::uint32_t* yp_tiles;  // near-phase row tiles per leaf
   std::uint32_t ncb, nodes;
   std::uint32_t signal_yp;        // the split leaf variant runs: Yp tiles are waited on
+  std::uint32_t fwd_signals;      // the producer lane publishes the stored tiles (wide DAGs)
 #ifdef HMXG_TRACE
   // diagnostic builds (tools/dag_trace.py): per claimed item, kTraceWords globaltimer stamps
   unsigned long long* trace;
@@ -641,6 +697,23 @@ __device__ __forceinline__ void spin_until(const std::uint32_t* p, std::uint32_t
     if (++polls > (1u << 24)) __trap();  // ~4 s: a missing dependency signal, not a slow tile
   }
 }
+// The producer lane's dependency wait: polls with a short backoff and forwards its own
+// CTA's finished tiles in between (`svc`), since the awaited tile may be one of them.
+template <class Svc>
+__device__ __forceinline__ void spin_until_svc(const std::uint32_t* p, std::uint32_t target, Svc&& svc) {
+  if (ld_acquire(p) >= target) return;
+  unsigned ns = 32;
+  std::uint32_t polls = 0;
+  while (ld_acquire(p) < target) {
+    svc();
+    __nanosleep(ns);
+    ns = min(ns * 2, 128u);
+    if (++polls > (1u << 25)) __trap();
+  }
+}
+__device__ __forceinline__ void red_release_gpu(std::uint32_t* counter, std::uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(counter), "r"(v) : "memory");
+}
 // A consumer warp has stored its part of an item: publish it. __syncwarp orders the
 // lanes' stores before lane 0's release-reduction at gpu scope (no CTA barrier, no L1
 // invalidating fence). Counters therefore count warps: targets are kConsumerWarps x items.
@@ -667,6 +740,29 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
+      // Forward the consumers' stored tiles (sig ring, in item order) to the done counters
+      // with a gpu-scope release: the consumer warps only arrive on a CTA-scope barrier
+      // after their stores, and go on to the next item instead of waiting for their stores
+      // to become visible to the whole GPU. Release is cumulative: the stores the
+      // consumers made before their arrive (acquired by the test below) are published.
+      // Narrow DAGs (few items per CTA) keep the consumers' own release: there the
+      // producer lane is the busier side, and its fences would delay its chunk issue.
+      std::uint32_t sig_seq = 0;
+      bool consumers_done = d.fwd_signals == 0;
+      auto service = [&]() {
+        while (!consumers_done) {
+          const int slot = sig_seq % kSigRing;
+          if (!mbar_test(&c.sfull[slot], (sig_seq / kSigRing) & 1)) return;
+          const std::uint64_t a = c.saddr[slot];
+          if (a == kSigEnd) {
+            consumers_done = true;
+            return;
+          }
+          if (a) red_release_gpu(reinterpret_cast<std::uint32_t*>(a), kConsumerWarps);
+          mbar_arrive(&c.sempty[slot]);
+          ++sig_seq;
+        }
+      };
       std::uint32_t it = 0;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t q = atomicAdd(d.claim, 1u);
@@ -678,28 +774,48 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
           tr[1] = gtimer();
         }
 #endif
-        post_item(c, seq, item);
+        post_item(c, seq, item, service);
         if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
         const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
         const Task task = p.tasks[static_cast<std::uint32_t>(item)];
         produce_gemm_tile(p, c, task, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
           if (sg.bbuf == kBufWp) return;  // Wp is complete: permute_in ran before this launch
-          spin_until((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
-                     d.node_tiles[sg.src] * kConsumerWarps);
+          spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
+                         d.node_tiles[sg.src] * kConsumerWarps, service);
           // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        });
+        }, service);
+        service();
         HMXG_STAMP(seq, 2);
+      }
+      std::uint32_t polls = 0;
+      while (!consumers_done) {  // the last tiles, up to the consumers' end record
+        service();
+        __nanosleep(64);
+        if (++polls > (1u << 26)) __trap();
       }
     }
     return;
   }
+  // consumer warps: hand an item's stored tile (or, with kSigEnd, the end) to the producer
+  auto post_signal = [&](std::uint32_t seq, std::uint64_t addr) {
+    __syncwarp();  // the warp's stores before lane 0's release arrive
+    if (lane == 0) {
+      const int slot = seq % kSigRing;
+      if (seq >= kSigRing) mbar_wait(&c.sempty[slot], ((seq / kSigRing) - 1) & 1);
+      if (warp == 0) c.saddr[slot] = addr;
+      mbar_arrive(&c.sfull[slot]);
+    }
+  };
 
   const FragAddr fa = frag_addresses(warp & 1, warp >> 1, lane >> 2, lane & 3);
   std::uint32_t it = 0;
   for (std::uint32_t seq = 0;; ++seq) {
     const std::uint64_t item = take_item(c, seq);
-    if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
+    if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) {
+      if (d.fwd_signals) post_signal(seq, kSigEnd);
+      break;
+    }
     const bool stamp = threadIdx.x == 0;
     if (stamp) HMXG_STAMP(seq, 3);
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
@@ -727,9 +843,13 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     });
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
-    if (task.cbuf != kBufYp || d.signal_yp)
-      warp_signal((task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
-                  static_cast<std::uint64_t>(task.node) * d.ncb + cb);
+    const bool publish = task.cbuf != kBufYp || d.signal_yp;
+    std::uint32_t* const ctr = (task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
+                               static_cast<std::uint64_t>(task.node) * d.ncb + cb;
+    if (d.fwd_signals)
+      post_signal(seq, publish ? reinterpret_cast<std::uint64_t>(ctr) : 0);
+    else if (publish)
+      warp_signal(ctr);
     if (stamp) HMXG_STAMP(seq, 5);
   }
 }
