@@ -345,8 +345,18 @@ constexpr int kTileRing = 4;
 // publishes them at gpu scope (kSigRing-deep ring: counter address, 0 = nothing, kSigEnd)
 constexpr int kSigRing = 8;
 constexpr std::uint64_t kSigEnd = ~std::uint64_t(0);
-constexpr int kSmemBytes =
-    kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * 8 + 3 * kSigRing * 8 + 1024;
+// A claimed work item as the producer hands it to the consumers: the item word, its task
+// and the task's first kSegSmem segment descriptors (the rest are read from global), so the
+// consumers start an item without global round trips for its tables.
+constexpr int kSegSmem = 6;
+struct RingSlot {
+  std::uint64_t item;
+  Task task;
+  SegDev seg[kSegSmem];
+};
+static_assert(sizeof(RingSlot) == 192, "RingSlot layout");
+constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * sizeof(RingSlot) +
+                           3 * kSigRing * 8 + 1024;
 
 struct CtaSmem {
   unsigned char* stage;    // kStages * kStageBytes, 1024-byte aligned
@@ -354,7 +364,7 @@ struct CtaSmem {
   std::uint64_t* empty;    // [kStages]
   std::uint64_t* tfull;    // [kTileRing]
   std::uint64_t* tempty;   // [kTileRing]
-  std::uint64_t* tring;    // [kTileRing] claimed work items
+  RingSlot* ring;          // [kTileRing] claimed work items
   std::uint64_t* sfull;    // [kSigRing] one arrive per consumer warp
   std::uint64_t* sempty;   // [kSigRing] the producer took the record
   std::uint64_t* saddr;    // [kSigRing]
@@ -368,8 +378,8 @@ __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
   c.empty = c.full + kStages;
   c.tfull = c.empty + kStages;
   c.tempty = c.tfull + kTileRing;
-  c.tring = c.tempty + kTileRing;
-  c.sfull = c.tring + kTileRing;
+  c.ring = reinterpret_cast<RingSlot*>(c.tempty + kTileRing);
+  c.sfull = reinterpret_cast<std::uint64_t*>(c.ring + kTileRing);
   c.sempty = c.sfull + kSigRing;
   c.saddr = c.sempty + kSigRing;
   return c;
@@ -394,35 +404,64 @@ __device__ __forceinline__ void init_barriers(const CtaSmem& c) {
   __syncthreads();
 }
 
-// Producer lane: post a claimed work item to the ring (waits for the slot to be free).
+// Producer lane: post a claimed work item to the ring (waits for the slot to be free) with
+// its task (`task_idx`, unless the item is the end) and first segment descriptors.
 template <class Svc = NoSvc>
-__device__ __forceinline__ void post_item(const CtaSmem& c, std::uint32_t seq, std::uint64_t item, Svc&& svc = Svc{}) {
+__device__ __forceinline__ RingSlot* post_item(const GemmParams& p, const CtaSmem& c, std::uint32_t seq,
+                                               std::uint64_t item, bool end, std::uint32_t task_idx,
+                                               Svc&& svc = Svc{}) {
   const int slot = seq % kTileRing;
+  RingSlot* rs = &c.ring[slot];
+  Task task{};
+  SegDev seg[kSegSmem];
+  if (!end) {  // loads first, so they overlap the wait for the slot
+    task = p.tasks[task_idx];
+    const std::uint32_t ns = min(task.seg_end - task.seg_begin, static_cast<std::uint32_t>(kSegSmem));
+#pragma unroll
+    for (int k = 0; k < kSegSmem; ++k)
+      if (k < static_cast<int>(ns)) seg[k] = p.segs[task.seg_begin + k];
+  }
   if (seq >= kTileRing) mbar_wait_svc(&c.tempty[slot], ((seq / kTileRing) - 1) & 1, svc);
-  c.tring[slot] = item;
-  mbar_arrive(&c.tfull[slot]);  // release: consumers read tring[slot] after their wait
+  rs->item = item;
+  if (!end) {
+    rs->task = task;
+    const std::uint32_t ns = min(task.seg_end - task.seg_begin, static_cast<std::uint32_t>(kSegSmem));
+#pragma unroll
+    for (int k = 0; k < kSegSmem; ++k)
+      if (k < static_cast<int>(ns)) rs->seg[k] = seg[k];
+  }
+  mbar_arrive(&c.tfull[slot]);  // release: consumers read the slot after their wait
+  return rs;
 }
 
-// Consumers: fetch the next work item from the ring.
-__device__ __forceinline__ std::uint64_t take_item(const CtaSmem& c, std::uint32_t seq) {
+// Consumers: the next work item's ring slot. It stays theirs until release_item (the
+// segment descriptors are read during the item).
+__device__ __forceinline__ const RingSlot* take_item(const CtaSmem& c, std::uint32_t seq) {
   const int slot = seq % kTileRing;
   mbar_wait(&c.tfull[slot], (seq / kTileRing) & 1);
-  const std::uint64_t item = c.tring[slot];
-  release_stage(&c.tempty[slot]);  // the ld.shared of the slot must retire first
-  return item;
+  return &c.ring[slot];
+}
+__device__ __forceinline__ void release_item(const CtaSmem& c, std::uint32_t seq) {
+  release_stage(&c.tempty[seq % kTileRing]);  // the slot's ld.shared must retire first
+}
+// Segment si of a task: from the ring slot for the first kSegSmem, else from global.
+__device__ __forceinline__ SegDev seg_at(const GemmParams& p, const RingSlot* rs, const Task& task, std::uint32_t si) {
+  const std::uint32_t k = si - task.seg_begin;
+  return k < static_cast<std::uint32_t>(kSegSmem) ? rs->seg[k] : p.segs[si];
 }
 
 // Producer lane: stream the A chunks and B tiles of one GEMM tile (column block cb).
 // `wait_dep(seg)` runs before a segment's first load (the DAG kernel's dependency wait; a
 // no-op per level).
 template <class WaitDep, class Svc = NoSvc>
-__device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
+__device__ __forceinline__ void produce_gemm_tile(const GemmParams& p, const CtaSmem& c, const RingSlot* rs,
                                                   std::uint32_t cb, const CUtensorMap* tm_wp, const CUtensorMap* tm_t,
                                                   const CUtensorMap* tm_s, std::uint32_t& it, WaitDep&& wait_dep,
                                                   Svc&& svc = Svc{}) {
   const int x = static_cast<int>(cb * kCbPitch);
+  const Task& task = rs->task;
   for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
-    const SegDev sg = p.segs[si];
+    const SegDev sg = seg_at(p, rs, task, si);
     wait_dep(sg);
     const CUtensorMap* map = sg.bbuf == kBufWp ? tm_wp : (sg.bbuf == kBufT ? tm_t : tm_s);
     for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch, ++it) {
@@ -463,9 +502,9 @@ struct NoHook {
   __device__ void operator()() const {}
 };
 template <class WaitId, class KEnd = NoHook>
-__device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const Task& task,
-                                                  std::uint32_t cb, const FragAddr& fa, std::uint32_t& it,
-                                                  WaitId&& wait_id, KEnd&& k_end = KEnd{}) {
+__device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const RingSlot* rs,
+                                                  const Task& task, std::uint32_t cb, const FragAddr& fa,
+                                                  std::uint32_t& it, WaitId&& wait_id, KEnd&& k_end = KEnd{}) {
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
@@ -541,7 +580,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
   // A segment may cover only the tile's first rows (SegDev::rows).
   const std::uint32_t base = smem_u32(c.stage);
   for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
-    const SegDev sg = p.segs[si];
+    const SegDev sg = seg_at(p, rs, task, si);
     const int rows = sg.rows ? static_cast<int>(sg.rows) : static_cast<int>(task.m);
     const int live_i = min(4, max(0, ((rows + 7) / 8 - wm + 1) / 2));
     const std::uint32_t nch = sg.nchunks;
@@ -604,10 +643,9 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
       std::uint32_t it = 0;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t t = atomicAdd(tile_counter, 1u);
-        post_item(c, seq, t);
+        const RingSlot* rs = post_item(p, c, seq, t, t >= ntiles, t / col_blocks);
         if (t >= ntiles) break;
-        produce_gemm_tile(p, c, p.tasks[t / col_blocks], t % col_blocks, &tm_wp, &tm_t, &tm_s, it,
-                          [](const SegDev&) {});
+        produce_gemm_tile(p, c, rs, t % col_blocks, &tm_wp, &tm_t, &tm_s, it, [](const SegDev&) {});
       }
     }
     return;
@@ -615,10 +653,16 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
   const FragAddr fa = frag_addresses(warp & 1, warp >> 1, lane >> 2, lane & 3);
   std::uint32_t it = 0;
   for (std::uint32_t seq = 0;; ++seq) {
-    const std::uint64_t t = take_item(c, seq);
-    if (t >= ntiles) break;
-    consume_gemm_tile(p, c, p.tasks[t / col_blocks], static_cast<std::uint32_t>(t % col_blocks), fa, it,
+    const RingSlot* rs = take_item(c, seq);
+    const std::uint64_t t = rs->item;
+    if (t >= ntiles) {
+      release_item(c, seq);
+      break;
+    }
+    const Task task = rs->task;
+    consume_gemm_tile(p, c, rs, task, static_cast<std::uint32_t>(t % col_blocks), fa, it,
                       [](const Task&, bool) {});  // the copied rows' level ran in an earlier launch
+    release_item(c, seq);
   }
 }
 
@@ -774,11 +818,11 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
           tr[1] = gtimer();
         }
 #endif
-        post_item(c, seq, item, service);
-        if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) break;
+        const bool end = static_cast<std::uint32_t>(item >> 56) == kItemEnd;
+        const RingSlot* rs = post_item(p, c, seq, item, end, static_cast<std::uint32_t>(item), service);
+        if (end) break;
         const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
-        const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-        produce_gemm_tile(p, c, task, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
+        produce_gemm_tile(p, c, rs, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
           if (sg.bbuf == kBufWp) return;  // Wp is complete: permute_in ran before this launch
           spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
                          d.node_tiles[sg.src] * kConsumerWarps, service);
@@ -811,16 +855,18 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   const FragAddr fa = frag_addresses(warp & 1, warp >> 1, lane >> 2, lane & 3);
   std::uint32_t it = 0;
   for (std::uint32_t seq = 0;; ++seq) {
-    const std::uint64_t item = take_item(c, seq);
+    const RingSlot* rs = take_item(c, seq);
+    const std::uint64_t item = rs->item;
     if (static_cast<std::uint32_t>(item >> 56) == kItemEnd) {
+      release_item(c, seq);
       if (d.fwd_signals) post_signal(seq, kSigEnd);
       break;
     }
     const bool stamp = threadIdx.x == 0;
     if (stamp) HMXG_STAMP(seq, 3);
     const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
-    const Task task = p.tasks[static_cast<std::uint32_t>(item)];
-    consume_gemm_tile(p, c, task, cb, fa, it, [&](const Task& t, bool own_rows) {
+    const Task task = rs->task;
+    consume_gemm_tile(p, c, rs, task, cb, fa, it, [&](const Task& t, bool own_rows) {
       // the rows about to be read are complete for this column block (every lane acquires;
       // the reads are plain L2 loads): the near phase's rows of this leaf, or the nodes
       // whose rows are copied (Wp is complete before the launch)
@@ -843,6 +889,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     });
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
+    release_item(c, seq);
     const bool publish = task.cbuf != kBufYp || d.signal_yp;
     std::uint32_t* const ctr = (task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
                                static_cast<std::uint64_t>(task.node) * d.ncb + cb;
