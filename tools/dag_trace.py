@@ -38,7 +38,7 @@ def trace(name: str, q: int | None = None) -> str:
 def summarize(path: str) -> None:
     rows = list(csv.DictReader(open(path)))
     for r in rows:
-        for k in ("t_claim", "t_issued", "t_take", "t_kend", "t_done"):
+        for k in ("t_claim", "t_issued", "t_take", "t_kend", "t_done", "t_first", "t_deps", "chunks"):
             r[k] = int(r[k])
     t0 = min(r["t_claim"] for r in rows)
     t1 = max(r["t_done"] for r in rows)
@@ -47,7 +47,8 @@ def summarize(path: str) -> None:
     for r in rows:
         ph[(int(r["kind"]), int(r["level"]))].append(r)
     order = sorted(ph, key=lambda k: min(r["t_claim"] for r in ph[k]))
-    print(f"{'phase':>9} {'items':>6} {'first':>8} {'last':>8} {'claim>take':>10} {'take>kend':>10} {'kend>done':>10}")
+    print(f"{'phase':>9} {'items':>6} {'chunks':>6} {'first':>8} {'last':>8} {'claim>take':>10} {'take>kend':>10} "
+          f"{'kend>done':>10} {'take>1st':>9} {'claim>deps':>10}")
     for k in order:
         rs = ph[k]
         n = len(rs)
@@ -56,7 +57,13 @@ def summarize(path: str) -> None:
         ct = sum(r["t_take"] - r["t_claim"] for r in rs) / n / 1e3
         tk = sum(r["t_kend"] - r["t_take"] for r in rs) / n / 1e3
         kd = sum(r["t_done"] - r["t_kend"] for r in rs) / n / 1e3
-        print(f"{KIND.get(k[0], k[0]):>6} L{k[1]:<2} {n:>6} {first:8.2f} {last:8.2f} {ct:10.2f} {tk:10.2f} {kd:10.2f}")
+        ch = sum(r["chunks"] for r in rs) / n
+        t1 = [r["t_first"] - r["t_take"] for r in rs if r["t_first"]]
+        t1 = sum(t1) / max(1, len(t1)) / 1e3
+        dp = [r["t_deps"] - r["t_claim"] for r in rs if r["t_deps"]]
+        dp = sum(dp) / len(dp) / 1e3 if dp else float("nan")
+        print(f"{KIND.get(k[0], k[0]):>6} L{k[1]:<2} {n:>6} {ch:6.1f} {first:8.2f} {last:8.2f} {ct:10.2f} {tk:10.2f} "
+              f"{kd:10.2f} {t1:9.2f} {dp:10.2f}")
 
 
 if __name__ == "__main__":
