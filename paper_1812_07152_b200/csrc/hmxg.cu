@@ -199,35 +199,42 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 // Work items of the whole-evaluation DAG launch for q columns, in topological order:
 // within a phase, row tiles in task order with the column block fastest (so a row tile's A
 // chunks are re-served from L2 to all column blocks).
-// With few column blocks the tree levels are too narrow to keep every SM busy, and the
-// split leaf variant is used: its near phase depends on Wp only, so its items are dealt
-// out in equal slices after every tree level but the first (CTAs that would wait for the
-// next level pick up near-field tiles instead), and the accumulating leaf phase comes
-// last. With many column blocks the Yp round trip of the split costs more than the idle
-// slots it fills (cfg5-HSS at Q=2048: +11% DAG time), so the combined leaf tasks run.
-constexpr std::uint32_t kSplitLeafMaxBlocks = 4;
-bool split_leaf(const Plan& plan, std::size_t q) {
-  return (q + kBN - 1) / kBN <= kSplitLeafMaxBlocks && !plan.split_phases.empty();
+// When the tree levels are too narrow to keep every CTA busy, the split leaf variant is
+// used: its near phase depends on Wp only, so its items are dealt out in equal slices
+// after every tree level but the first (CTAs that would wait for the next level pick up
+// near-field tiles instead), and the accumulating leaf phase comes last. Otherwise the Yp
+// round trip of the split costs more than the idle slots it fills, and the combined leaf
+// tasks run. The criterion is work items per CTA of the combined variant (measured:
+// cfg1 Q=64, 0.4 per CTA, and cfg2 Q=256, 32: split faster; cfg5-HSS Q=256, 83: combined
+// 1.81 vs 1.89 ms; Q=2048, 660: combined, split +11%). Both variants give the same bits.
+#ifndef HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA
+#define HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA 48
+#endif
+bool split_leaf(const Plan& plan, std::size_t q, unsigned grid) {
+  if (plan.split_phases.empty()) return false;
+  std::uint64_t tasks = 0;
+  for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
+  return tasks * ((q + kBN - 1) / kBN) < std::uint64_t(HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA) * grid;
 }
 // The level-by-level launch sequence for q columns (HMXG_F_LEVEL_LAUNCHES): the same leaf
 // variant as the DAG launch, so both give the same bits.
-std::vector<const Phase*> level_phases(const Plan& plan, std::size_t q) {
+std::vector<const Phase*> level_phases(const Plan& plan, std::size_t q, unsigned grid) {
   std::vector<const Phase*> out;
-  const bool split = split_leaf(plan, q);
+  const bool split = split_leaf(plan, q, grid);
   for (const Phase& ph : plan.phases)
     if (!(split && ph.kind == kPhaseLeaf)) out.push_back(&ph);
   if (split)
     for (const Phase& ph : plan.split_phases) out.push_back(&ph);
   return out;
 }
-std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage) {
+std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage, unsigned grid) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
   std::vector<std::uint64_t> items;
   auto emit = [&](std::uint32_t t0, std::uint32_t t1) {
     for (std::uint32_t t = t0; t < t1; ++t)
       for (std::uint32_t cb = 0; cb < ncb; ++cb) items.push_back(make_item(kItemGemm, cb, t));
   };
-  const bool split = split_leaf(plan, q);
+  const bool split = split_leaf(plan, q, grid);
   std::vector<const Phase*> tree, leaf;
   const Phase* near = nullptr;
   for (const Phase& ph : plan.phases) {
@@ -263,7 +270,12 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
 // eval_dag's producer lanes publish the stored tiles when every CTA runs many items
 // (cfg5-HSS, 660 per CTA: DAG -1.4%); with few (cfg2, 32 per CTA) the producer is the busier
 // side and the consumers release their own tiles (forwarding cost cfg2 +21%).
-std::uint32_t forward_signals(std::uint32_t nitems, unsigned grid) { return nitems >= 128ull * grid ? 1u : 0u; }
+#ifndef HMXG_FWD_MIN_ITEMS_PER_CTA
+#define HMXG_FWD_MIN_ITEMS_PER_CTA 128
+#endif
+std::uint32_t forward_signals(std::uint32_t nitems, unsigned grid) {
+  return nitems >= std::uint64_t(HMXG_FWD_MIN_ITEMS_PER_CTA) * grid ? 1u : 0u;
+}
 
 // [claim counter per stage | T counters | S counters | Yp counters] (nodes x ncb each)
 constexpr std::size_t kDagClaimWords = 2;
@@ -284,7 +296,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   HMXG_CUDA(cudaStreamSynchronize(st));  // the slot's previous list may still be in use
   cudaFree(e.items);
   e = DevState::DagItems{};
-  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage);
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage, d.gemm_grid);
   if (items.size() >= 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many work items");
   HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
   const std::size_t words = dag_done_words(plan, q);
@@ -317,13 +329,13 @@ int trace_prepare(const DevState& d, cudaStream_t st) {
   HMXG_CUDA(cudaMemsetAsync(g_trace, 0, words * sizeof(unsigned long long), st));
   return HMXG_OK;
 }
-void trace_dump(const Plan& plan, std::size_t q) {
+void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
   const char* path = std::getenv("HMXG_TRACE_OUT");
   if (!path || !g_trace) return;
   std::vector<unsigned long long> h(g_trace_words);
   if (cudaMemcpy(h.data(), g_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return;
-  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0);
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
   std::vector<const Phase*> phs;
   for (const Phase& ph : plan.phases) phs.push_back(&ph);
   for (const Phase& ph : plan.split_phases) phs.push_back(&ph);
@@ -405,7 +417,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.done = d.dag_done + kDagClaimWords;
     dp.node_tiles = d.node_tiles;
     dp.yp_tiles = d.yp_tiles;
-    dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
+    dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
     dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);
@@ -439,7 +451,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   ++*launches;
   HMXG_TRY(mark());
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
-  const std::vector<const Phase*> lphases = level_phases(plan, q);
+  const std::vector<const Phase*> lphases = level_phases(plan, q, d.gemm_grid);
   HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, lphases.size() * sizeof(std::uint32_t), st));
   for (std::size_t ph_i = 0; ph_i < lphases.size(); ++ph_i) {
     const Phase& ph = *lphases[ph_i];
@@ -817,7 +829,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.done = d.dag_done + kDagClaimWords;
   dp.node_tiles = d.node_tiles;
   dp.yp_tiles = d.yp_tiles;
-  dp.signal_yp = split_leaf(plan, q) ? 1u : 0u;
+  dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
   dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);
@@ -901,14 +913,14 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
 int hmxg_phase_count(const hmxg_mat* mat) {
   if (!mat) return -1;
   const DevState& d = mat->devs[0];
-  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q).size() + 2) : 3;
+  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q, d.gemm_grid).size() + 2) : 3;
 }
 
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
   const Plan& p = mat->plan;
   const bool levels = mat->devs[0].last_levels;
-  const std::vector<const Phase*> lphases = level_phases(p, mat->devs[0].last_q);
+  const std::vector<const Phase*> lphases = level_phases(p, mat->devs[0].last_q, mat->devs[0].gemm_grid);
   const std::uint32_t count = static_cast<std::uint32_t>(levels ? lphases.size() + 2 : 3);
   if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
   std::memset(out, 0, sizeof *out);
@@ -1005,7 +1017,7 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       HMXG_CUDA(cudaEventSynchronize(d.ev1));
       HMXG_CUDA(cudaEventElapsedTime(&dev_ms, d.ev0, d.ev1));
 #ifdef HMXG_TRACE
-      if (!levels) trace_dump(plan, q);
+      if (!levels) trace_dump(plan, q, d.gemm_grid);
 #endif
     }
   } else {

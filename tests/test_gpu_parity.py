@@ -136,16 +136,16 @@ def test_device_pointer_path():
     assert np.array_equal(y, ev.evaluate(w))
 
 
-@pytest.mark.parametrize("name", ["cfg2-h2b", "cfg1-hss"])
-def test_leaf_variants_give_the_same_bits(name):
-    """Wide Q on the device runs the combined leaf tasks; the host path evaluates 64-column
-    chunks, which run the split leaf variant (near tasks, then V_i S_i accumulated). Both
-    sum every row in one order, so the results are equal bit for bit."""
+@pytest.mark.parametrize("name,q", [("cfg5-hss", 320), ("cfg2-h2b", 1024)])
+def test_leaf_variants_give_the_same_bits(name, q):
+    """Wide Q on the device runs the combined leaf tasks (≥48 work items per CTA); the host
+    path evaluates 64-column chunks, which run the split leaf variant (near tasks, then
+    V_i S_i accumulated). Both sum every row in one order: equal bit for bit."""
     import torch
 
     spec, _ = config(name)
     inst = build_instance(spec)
-    n, q = inst.cds.n, 320  # 5 column blocks: combined leaf tasks on the device path
+    n = inst.cds.n
     ev = Evaluator(inst.cds)
     w = _w(n, q, 8)
     wd = torch.from_numpy(w.T.copy()).cuda()
@@ -155,7 +155,8 @@ def test_leaf_variants_give_the_same_bits(name):
     y_dev = yd.cpu().numpy().T
     assert np.array_equal(y_dev, ev.evaluate(w))
     assert np.array_equal(y_dev, ev.evaluate(w, levels=True))
-    assert oracle.rel_frob(y_dev, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    cols = np.arange(0, q, q // 16)
+    assert oracle.rel_frob(y_dev[:, cols], oracle.oracle_evaluate(inst.cds, np.asfortranarray(w[:, cols]))) <= TOL
 
 
 def test_graph_replay_matches_direct_launches():
@@ -221,7 +222,7 @@ def test_dag_launch_equals_level_launches(name, q):
 
 @pytest.mark.parametrize("q", [1, 7, 63, 65, 129, 257, 320])
 def test_ragged_column_counts(q):
-    """Every column count, narrow (split leaf variant, ≤4 blocks) and wide, partial last
+    """Every column count, one to several column blocks, partial last
     blocks included: the oracle's result, and the DAG equal to the level launches."""
     inst = build_instance(InstanceSpec(n=3000, d=3, leaf=48, max_rank=40, mode="tau", tau=0.7, seed=12))
     ev = Evaluator(inst.cds)
