@@ -272,9 +272,10 @@ def ours(args) -> None:
     def step(time_phases=False):
         ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=stream.cuda_stream, time_phases=time_phases)
 
+    # warm up with the same graph the timed steps replay (captured with per-launch events)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            step()
+            step(time_phases=True)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region

@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hmxg.h"
@@ -77,9 +78,10 @@ struct DevState {
     cudaStream_t st = nullptr;
     const double* wp = nullptr;
     bool levels = false;
+    bool timed = false;  // captured with per-launch event nodes (and without programmatic launch)
     bool operator==(const GraphKey& o) const {
       return w == o.w && y == o.y && q == o.q && ldw == o.ldw && ldy == o.ldy && st == o.st && wp == o.wp &&
-             levels == o.levels;
+             levels == o.levels && timed == o.timed;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
@@ -369,6 +371,25 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
 
 // Default: one whole-evaluation DAG launch. `levels`: the level-by-level launch sequence
 // (permute-in, one launch per tree level, permute-out) for per-launch breakdowns.
+// A launch that may overlap its predecessor (programmatic dependent launch): the kernel
+// waits for it in-kernel (griddepcontrol.wait). pdl false: an ordinary stream launch.
+template <class... KArgs, class... Args>
+int launch_dependent(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  HMXG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return HMXG_OK;
+}
+
 int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw, double* y,
                  std::size_t ldy, std::size_t q, cudaStream_t st, bool time_phases, bool levels,
                  std::uint32_t* launches) {
@@ -376,14 +397,14 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   const std::uint32_t qq = static_cast<std::uint32_t>(q);
   const dim3 eblk(256);
   d.last_q = q;
-  // Per-launch timing events. Under graph capture they become external event-record
-  // nodes, so a replayed graph still times every launch.
+  // Per-launch timing events (time_phases). Under graph capture they become external
+  // event-record nodes, so a replayed timed graph still times every launch.
   std::size_t ev = 0;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   HMXG_CUDA(cudaStreamIsCapturing(st, &cap));
   const bool capturing = cap == cudaStreamCaptureStatusActive;
   auto mark = [&]() -> int {
-    if (time_phases || capturing)
+    if (time_phases)
       HMXG_CUDA(cudaEventRecordWithFlags(d.phase_ev[ev++], st, capturing ? cudaEventRecordExternal : 0u));
     return HMXG_OK;
   };
@@ -426,28 +447,32 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     HMXG_TRY(trace_prepare(d, st));
     dp.trace = g_trace;
 #endif
-    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
     HMXG_TRY(mark());
     const dim3 pgrid2((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
     if (pgrid2.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
-    permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
+    // permute_in also zeroes the DAG's counters; eval_dag and permute_out are programmatic
+    // dependent launches (their launch overlaps the predecessor; they wait in-kernel). With
+    // per-launch timing the dependents launch normally, so each event brackets one kernel.
+    permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, d.dag_done, dag_done_words(plan, q));
     ++*launches;
     HMXG_TRY(mark());
+    const bool pdl = !time_phases;  // an event between two kernels would break the programmatic edge
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
-    eval_dag<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+    HMXG_TRY(launch_dependent(pdl, eval_dag, dim3(grid), dim3(kThreads), kSmemBytes, st, tm_wp, tm_t, tm_s, p, dp));
     ++*launches;
     HMXG_TRY(mark());
-    permute_out<<<pgrid2, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq);
+    HMXG_TRY(launch_dependent(pdl, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp), std::uint64_t(ldq),
+                              static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n, qq));
     ++*launches;
     HMXG_TRY(mark());
     HMXG_CUDA(cudaGetLastError());
-    if (time_phases || capturing) d.phase_valid = true;
+    if (time_phases) d.phase_valid = true;
     return HMXG_OK;
   }
   HMXG_TRY(mark());
   const dim3 pgrid((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
   if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
-  permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq);
+  permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, nullptr, 0);
   ++*launches;
   HMXG_TRY(mark());
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
@@ -468,7 +493,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   ++*launches;
   HMXG_TRY(mark());
   HMXG_CUDA(cudaGetLastError());
-  if (time_phases || capturing) d.phase_valid = true;
+  if (time_phases) d.phase_valid = true;
   return HMXG_OK;
 }
 
@@ -845,7 +870,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
     HMXG_CUDA(cudaMemsetAsync(d.t, 0, plan.skel_rows * ldq * sizeof(double), st));
     HMXG_CUDA(cudaMemsetAsync(d.yp, 0, plan.rows_pad * ldq * sizeof(double), st));
     HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
-    permute_in<<<pgrid, 256, 0, st>>>(W, ldw, d.ipmap, d.wp, ldq, nn, qq);
+    permute_in<<<pgrid, 256, 0, st>>>(W, ldw, d.ipmap, d.wp, ldq, nn, qq, nullptr, 0);
   } else if (!plan.remote_t_nodes.empty()) {
     // T of the other parts' nodes arrived through the exchange: mark it complete
     const std::uint64_t cells = std::uint64_t(plan.remote_t_nodes.size()) * ncb;
@@ -990,13 +1015,13 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread || (flags & HMXG_F_NO_GRAPH)) {
       HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &launches));
     } else {
-      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, levels};
+      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, levels, time_phases};
       if (!(d.gexec && d.gkey == key)) {
         d.drop_graph();
         cudaGraph_t graph = nullptr;
         HMXG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         std::uint32_t captured = 0;
-        const int rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, false, levels, &captured);
+        const int rc = enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &captured);
         const cudaError_t ec = cudaStreamEndCapture(st, &graph);
         if (rc != HMXG_OK) {
           if (graph) cudaGraphDestroy(graph);

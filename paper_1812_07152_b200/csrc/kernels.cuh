@@ -167,6 +167,14 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch (the DAG path launches eval_dag and permute_out with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a dependent grid may start while
+// its predecessor runs and waits here before reading the predecessor's output; the
+// predecessor lets it launch once all of its own CTAs are running. Both are no-ops for
+// grids launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
 // Uniform selects instead of dynamic indexing into parameter arrays (no local copies).
 __device__ __forceinline__ double* pick_buf(const GemmParams& p, unsigned b) {
   return b == kBufWp ? p.buf[kBufWp] : (b == kBufT ? p.buf[kBufT] : (b == kBufS ? p.buf[kBufS] : p.buf[kBufYp]));
@@ -777,6 +785,8 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   extern __shared__ unsigned char smem_raw[];
   const CtaSmem c = carve_smem(smem_raw);
   init_barriers(c);
+  pdl_trigger();  // permute_out may launch; it waits for this grid before reading Yp
+  pdl_wait();     // Wp and the zeroed counters of permute_in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   std::uint32_t* const done_t = d.done;
   std::uint32_t* const done_s = done_t + static_cast<std::uint64_t>(d.nodes) * d.ncb;
@@ -911,16 +921,26 @@ __global__ void preset_done(const std::uint32_t* __restrict__ nodes, std::uint32
   done_t[static_cast<std::uint64_t>(node) * ncb + cb] = node_tiles[node] * kConsumerWarps;
 }
 
+
 // Transpose-permute into the point-major internal layout: Wp[ipmap[r], c] = W[r, c]
 // (column c at physical column phys_col(c)).
 // A 32 x 32 tile is read column by column (256 B contiguous per column of W), turned
 // around in shared memory and written row by row (256 B contiguous per point row of Wp),
 // so both sides move whole cache lines although the rows land in permuted order.
 constexpr int kTT = 32;
+// `zero` (optional): words the next launch needs zeroed (eval_dag's claim and completion
+// counters), cleared here instead of by a separate memset node; the blocks split them.
 __global__ void __launch_bounds__(256) permute_in(const double* __restrict__ w, std::uint64_t ldw,
                                                   const std::uint32_t* __restrict__ ipmap, double* __restrict__ wp,
-                                                  std::uint64_t ldwp, std::uint32_t n, std::uint32_t q) {
+                                                  std::uint64_t ldwp, std::uint32_t n, std::uint32_t q,
+                                                  std::uint32_t* __restrict__ zero, std::uint64_t nzero) {
   __shared__ double tile[kTT][kTT + 1];
+  pdl_trigger();
+  if (zero) {
+    const std::uint64_t nb = static_cast<std::uint64_t>(gridDim.x) * gridDim.y;
+    const std::uint64_t b = blockIdx.y * static_cast<std::uint64_t>(gridDim.x) + blockIdx.x;
+    for (std::uint64_t i = b * blockDim.x + threadIdx.x; i < nzero; i += nb * blockDim.x) zero[i] = 0u;
+  }
   const std::uint32_t r0 = blockIdx.x * kTT, c0 = blockIdx.y * kTT;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
 #pragma unroll
@@ -941,6 +961,7 @@ __global__ void __launch_bounds__(256) permute_out(const double* __restrict__ yp
                                                    const std::uint32_t* __restrict__ ipmap, double* __restrict__ y,
                                                    std::uint64_t ldy, std::uint32_t n, std::uint32_t q) {
   __shared__ double tile[kTT][kTT + 1];
+  pdl_wait();  // Yp is complete (a no-op without programmatic launch)
   const std::uint32_t r0 = blockIdx.x * kTT, c0 = blockIdx.y * kTT;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll

@@ -238,7 +238,7 @@ int kernel_rows_dev(hmxg_points& P, const std::uint32_t* rows, std::uint64_t nro
   // rows n .. npad of Wt meet the zero A columns past the last point; clear what an
   // earlier call with another pitch may have left there
   if (npad > n) HMXG_CUDA(cudaMemsetAsync(P.wt + n * ldq, 0, (npad - n) * ldq * sizeof(double), st));
-  permute_in<<<tgrid, 256, 0, st>>>(w, ldw, P.ident, P.wt, ldq, static_cast<std::uint32_t>(n), qq);
+  permute_in<<<tgrid, 256, 0, st>>>(w, ldw, P.ident, P.wt, ldq, static_cast<std::uint32_t>(n), qq, nullptr, 0);
   ++*launches;
   if (rows) {
     HMXG_CUDA(cudaStreamSynchronize(st));
