@@ -507,12 +507,14 @@ __device__ __forceinline__ FragAddr frag_addresses(int wm, int wn, int fr, int f
 // `wait_id(task)` runs before the identity rows are read (the DAG kernel's wait for the
 // nodes that produce them; a no-op per level, where they ran in an earlier launch).
 struct NoHook {
-  __device__ void operator()() const {}
+  template <class... A>
+  __device__ void operator()(A...) const {}
 };
-template <class WaitId, class KEnd = NoHook>
+template <class WaitId, class KEnd = NoHook, class KStart = NoHook>
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const RingSlot* rs,
                                                   const Task& task, std::uint32_t cb, const FragAddr& fa,
-                                                  std::uint32_t& it, WaitId&& wait_id, KEnd&& k_end = KEnd{}) {
+                                                  std::uint32_t& it, WaitId&& wait_id, KEnd&& k_end = KEnd{},
+                                                  KStart&& k_start = KStart{}) {
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
@@ -587,6 +589,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
   // uniformly, once per segment) to a K loop instantiated for their live fragment count.
   // A segment may cover only the tile's first rows (SegDev::rows).
   const std::uint32_t base = smem_u32(c.stage);
+  k_start(it);
   for (std::uint32_t si = task.seg_begin; si < task.seg_end; ++si) {
     const SegDev sg = seg_at(p, rs, task, si);
     const int rows = sg.rows ? static_cast<int>(sg.rows) : static_cast<int>(task.m);
@@ -706,7 +709,7 @@ struct DagParams {
 #ifdef HMXG_TRACE
 // per (CTA, claim sequence): smid << 32 | item index, claim, producer issued the item's last
 // chunk, consumer warp 0 took the item, its K loop ended, its tile was stored and signalled
-constexpr int kTraceWords = 6;
+constexpr int kTraceWords = 8;  // + [6] first chunk ready (consumer), [7] deps met (producer)
 constexpr int kTraceSeq = 4096;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -838,6 +841,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
                          d.node_tiles[sg.src] * kConsumerWarps, service);
           // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          HMXG_STAMP(seq, 7);
         }, service);
         service();
         HMXG_STAMP(seq, 2);
@@ -896,6 +900,15 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
                    d.node_tiles[node] * kConsumerWarps);
     }, [&]() {
       if (stamp) HMXG_STAMP(seq, 4);
+    }, [&](std::uint32_t it0) {
+#ifdef HMXG_TRACE
+      if (task.seg_end > task.seg_begin) {  // trace builds: when the first chunk is ready
+        mbar_wait(&c.full[it0 % kStages], (it0 / kStages) & 1);
+        if (stamp) HMXG_STAMP(seq, 6);
+      }
+#else
+      (void)it0;
+#endif
     });
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
