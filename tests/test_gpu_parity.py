@@ -242,3 +242,34 @@ def test_tiny_trees(n, leaf):
     y = evaluate(inst.cds, EvalPlan(), w)
     assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w)) <= TOL
     inst.close()
+
+
+@pytest.mark.parametrize("devices", [(0,), (0, 0)])
+def test_strided_w_and_y(devices):
+    """Leading dimensions larger than n (odd ones included) on the host-pointer path (one
+    device and two column shards) and the device-pointer path: the same bits as compact
+    buffers, and the rows of Y past n are left untouched."""
+    import torch
+
+    inst = build_instance(InstanceSpec(n=3000, d=3, leaf=48, max_rank=40, mode="tau", tau=0.7, seed=12))
+    n, q = inst.cds.n, 70
+    ev = Evaluator(inst.cds, devices=devices)
+    w = _w(n, q, 31)
+    y_ref = ev.evaluate(w)
+    ldw, ldy = n + 5, n + 3
+    wbig = np.asfortranarray(np.full((ldw, q), np.nan))
+    wbig[:n] = w
+    ybig = np.asfortranarray(np.full((ldy, q), -7.0))
+    ev.evaluate_host_ptr(wbig.ctypes.data, ybig.ctypes.data, q, ldw=ldw, ldy=ldy)
+    assert np.array_equal(ybig[:n], y_ref)
+    assert np.all(ybig[n:] == -7.0)
+    if len(devices) == 1:
+        wd = torch.from_numpy(wbig.T.copy()).cuda()  # (q, ldw) row major == ldw x q column major
+        yd = torch.full((q, ldy), -7.0, dtype=torch.float64, device="cuda")
+        ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, ldw=ldw, ldy=ldy, stream=torch_stream())
+        torch.cuda.synchronize()
+        yh = yd.cpu().numpy().T
+        assert np.array_equal(yh[:n], y_ref)
+        assert np.all(yh[n:] == -7.0)
+    ev.close()
+    inst.close()
