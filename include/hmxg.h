@@ -37,13 +37,16 @@ extern "C" {
 #define HMXG_F_NO_SYNC 0x2u     /* with DEVICE_PTRS: enqueue on `stream` and return */
 #define HMXG_F_NO_GRAPH 0x8u    /* with DEVICE_PTRS: issue the launches instead of replaying the
                                    cached CUDA graph of the launch sequence (the graph is keyed
-                                   on W, Y, q, leading dimensions and a non-NULL stream) */
+                                   on W, Y, q, leading dimensions, a non-NULL stream and
+                                   HMXG_F_TIME_PHASES) */
 #define HMXG_F_LEVEL_LAUNCHES 0x10u /* run the level-by-level launch sequence (one launch per
                                        tree level) instead of the single whole-evaluation DAG
                                        launch: same results, per-launch timing breakdown */
-#define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0; graph
-                                   replays always record them);
-                                   read back with hmxg_phase_get */
+#define HMXG_F_TIME_PHASES 0x4u /* record a CUDA event pair around every launch (device 0; a
+                                   graph captured with it keeps them as event nodes);
+                                   read back with hmxg_phase_get. Without it, eval_dag and
+                                   permute-out are programmatic dependent launches (their
+                                   launch overlaps the preceding kernel) */
 
 /*
  * View of a computation-ordered CDS (reference struct hmx::CDS,
