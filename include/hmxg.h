@@ -146,6 +146,12 @@ int hmxg_free(hmxg_mat* mat);
  * success, if info != NULL, the size fields (n, *_elems, skel_rows, launches_per_eval,
  * flops_per_col) are filled. */
 int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info);
+/* Host-only check of the whole-evaluation DAG launch for q columns and a grid of `grid`
+ * resident CTAs (no device needed): the claim order holds every task tile of the leaf
+ * variant that runs exactly once, every tile an item waits for (B operand rows, identity
+ * rows, the split leaf tasks' near rows) comes before it, and the completion targets equal
+ * the writer tile counts. These are what eval_dag's deadlock freedom rests on. */
+int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* nitems);
 int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info);
 
 /* Subtree-split fallback for a CDS larger than one GPU's HBM. Part `part` of

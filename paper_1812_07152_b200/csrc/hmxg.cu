@@ -774,6 +774,74 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
 }
 
 
+int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* nitems) {
+  if (!cds || q == 0 || grid == 0) return set_err(HMXG_EINVAL, "hmxg_dag_check: null view, q = 0 or grid = 0");
+  Plan plan;
+  std::string err;
+  if (!build_plan(*cds, kBM, plan, err)) return set_err(HMXG_EINVAL, err);
+  const std::uint32_t ncb = static_cast<std::uint32_t>((q + kBN - 1) / kBN);
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
+  if (nitems) *nitems = items.size();
+  const bool split = split_leaf(plan, q, grid);
+  // (1) every task of the variant that runs, once per column block
+  std::vector<std::uint32_t> want(plan.tasks.size(), 0), seen(plan.tasks.size() * std::size_t(ncb), 0);
+  for (const Phase& ph : plan.phases)
+    if (!(split && ph.kind == kPhaseLeaf))
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) want[t] = 1;
+  if (split)
+    for (const Phase& ph : plan.split_phases)
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) want[t] = 1;
+  std::vector<std::uint8_t> is_near(plan.tasks.size(), 0);
+  for (const Phase& ph : plan.split_phases)
+    if (ph.kind == kPhaseNear)
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) is_near[t] = split ? 1 : 0;
+  for (std::uint64_t it : items) {
+    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = static_cast<std::uint32_t>(it >> 32) & 0xffffffu;
+    if (t >= plan.tasks.size() || cb >= ncb || !want[t] || seen[std::size_t(t) * ncb + cb]++)
+      return set_err(HMXG_EINVAL, "dag: item list is not the variant's tasks x column blocks");
+  }
+  for (std::size_t t = 0; t < plan.tasks.size(); ++t)
+    for (std::uint32_t cb = 0; cb < ncb; ++cb)
+      if (want[t] && !seen[t * ncb + cb]) return set_err(HMXG_EINVAL, "dag: a task tile is missing");
+  // (3) the kernel's completion targets are the writer counts
+  const std::size_t nn = plan.num_nodes;
+  std::vector<std::uint32_t> wr(3 * nn, 0);
+  for (std::size_t t = 0; t < plan.tasks.size(); ++t) {
+    if (!want[t]) continue;
+    const Task& tk = plan.tasks[t];
+    if (tk.cbuf == kBufT) ++wr[tk.node];
+    if (tk.cbuf == kBufS) ++wr[nn + tk.node];
+    if (is_near[t]) ++wr[2 * nn + tk.node];
+  }
+  for (std::size_t i = 0; i < nn; ++i) {
+    if (wr[i] && wr[i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: T target != writer tiles");
+    if (wr[nn + i] && wr[nn + i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: S target != writer tiles");
+    if (split && wr[2 * nn + i] != plan.yp_tiles[i]) return set_err(HMXG_EINVAL, "dag: Yp target != near tiles");
+  }
+  // (2) topological: every tile an item waits for is complete before it in the claim order
+  std::vector<std::uint32_t> done(3 * nn * std::size_t(ncb), 0);
+  auto ready = [&](std::size_t r, std::uint32_t cb) { return done[r * ncb + cb] >= wr[r]; };
+  for (std::uint64_t it : items) {
+    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = static_cast<std::uint32_t>(it >> 32) & 0xffffffu;
+    const Task& tk = plan.tasks[t];
+    for (std::uint32_t sgi = tk.seg_begin; sgi < tk.seg_end; ++sgi) {
+      const SegDev& sg = plan.segs[sgi];
+      if ((sg.bbuf == kBufT || sg.bbuf == kBufS) && !ready((sg.bbuf == kBufT ? 0 : nn) + sg.src, cb))
+        return set_err(HMXG_EINVAL, "dag: an item precedes the tiles its B operand reads");
+    }
+    if (tk.id_off != kNoMap && (tk.id_buf == kBufT || tk.id_buf == kBufS))
+      for (std::uint32_t nd : {tk.id_node0, tk.id_node1})
+        if (nd != kNoMap && !ready((tk.id_buf == kBufT ? 0 : nn) + nd, cb))
+          return set_err(HMXG_EINVAL, "dag: an item precedes the tiles its identity rows copy");
+    if ((tk.flags & kTaskAccumulate) && !ready(2 * nn + tk.node, cb))
+      return set_err(HMXG_EINVAL, "dag: a leaf task precedes its near tiles");
+    if (tk.cbuf == kBufT) ++done[std::size_t(tk.node) * ncb + cb];
+    if (tk.cbuf == kBufS) ++done[(nn + tk.node) * ncb + cb];
+    if (is_near[t]) ++done[(2 * nn + tk.node) * ncb + cb];
+  }
+  return HMXG_OK;
+}
+
 int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
   return upload_impl(ctx, cds, SplitSpec{}, out);
 }

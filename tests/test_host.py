@@ -229,3 +229,40 @@ def test_identity_rows_lowering_counts():
     assert unit > 0
     assert info.exec_flops_per_col == pytest.approx(info.flops_per_col - 2 * 2 * unit, rel=1e-12)
     inst.close()
+
+
+@pytest.mark.parametrize("q,grid", [(1, 444), (64, 444), (65, 444), (256, 444), (2048, 444), (256, 4), (256, 100000)])
+def test_dag_claim_order_is_topological(q, grid):
+    """eval_dag's deadlock freedom (DESIGN, Kernels): in the claim order every tile an item
+    waits for comes first, each task tile of the leaf variant that runs appears once, and
+    the completion targets equal the writer tile counts. Host-only (hmxg_dag_check); the
+    grid sizes pick the combined (few CTAs) or split (many CTAs) leaf variant."""
+    insts = [_small(),
+             build_instance(InstanceSpec(n=3000, d=3, leaf=48, max_rank=40, mode="tau", tau=0.7, seed=12)),
+             build_instance(InstanceSpec(n=2000, d=2, leaf=32, max_rank=16, seed=5))]
+    for inst in insts:
+        v = inst.cds.view()
+        n_items = C.c_uint64()
+        rc = N.hmxg().hmxg_dag_check(C.byref(v), q, grid, C.byref(n_items))
+        assert rc == 0, N.last_error(N.hmxg(), "hmxg")
+        assert n_items.value > 0
+        inst.close()
+
+
+def test_dag_claim_order_reference_instance():
+    ri = oracle.RefInstance(oracle.RefInstanceSpec(n=460, d=8, mode=0, tau=0.65, leaf=16, max_rank=24, seed=4))
+    v = ri.cds.view()
+    for q, grid in [(7, 444), (130, 444), (130, 2)]:
+        assert N.hmxg().hmxg_dag_check(C.byref(v), q, grid, None) == 0, N.last_error(N.hmxg(), "hmxg")
+
+
+@pytest.mark.parametrize("name", ["cfg1-hss", "cfg2-h2b"])
+def test_dag_claim_order_baseline_configs(name):
+    from paper_1812_07152_b200 import config
+
+    spec, q = config(name)
+    inst = build_instance(spec)
+    v = inst.cds.view()
+    for qq in (q, 4 * q):
+        assert N.hmxg().hmxg_dag_check(C.byref(v), qq, 444, None) == 0, N.last_error(N.hmxg(), "hmxg")
+    inst.close()
