@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -30,8 +31,30 @@ int make_map(CUtensorMap* map, const double* base, std::uint64_t rows, std::uint
 }
 
 // Columns per pipeline chunk of the host-pointer path: H2D of chunk k+1 and D2H of chunk
-// k-1 overlap the evaluation of chunk k.
+// k-1 overlap the evaluation of chunk k. When PCIe bounds the pipeline (cfg5-HSS), 64: a
+// wider chunk only lengthens the unhidden first copy-in and last copy-out. When the
+// evaluation does (its executed FP64 work at ~30 TF/s is over twice the W and Y bytes at
+// ~45 GB/s per direction), each chunk also pays a fixed cost c of about 0.4 ms (the top
+// of the tree and the launches: measured 0.3-0.45 ms on cfg3-cfg5-H2-b), and the width
+// balances the two: w* = sqrt(Q c 45e9 / (16 n)), rounded to 64 x a power of two, at most
+// 256. Measured e2e: cfg3 35.8 -> 33.6 ms (w 128), cfg5-H2-b 299 -> 296 ms (w 128); cfg4
+// stays at 64 (w 256 cost +4%).
 constexpr std::size_t kChunkCols = 64;
+std::size_t host_chunk_cols(const Plan& plan, std::size_t qg) {
+#ifndef HMXG_HOST_CHUNK_ADAPTIVE
+#define HMXG_HOST_CHUNK_ADAPTIVE 1
+#endif
+  if (!HMXG_HOST_CHUNK_ADAPTIVE) return std::min(qg, kChunkCols);
+  double flops_per_col = 0.0;
+  for (const Phase& ph : plan.phases) flops_per_col += ph.flops_per_col;
+  const double bw = 45e9, per_chunk = 0.4e-3;
+  const double compute = flops_per_col / 30e12, transfer = 8.0 * double(plan.n) / bw;  // per column
+  if (compute < 2.0 * transfer) return std::min(qg, kChunkCols);
+  const double w = std::sqrt(double(qg) * per_chunk * bw / (16.0 * double(plan.n)));
+  std::size_t cols = kChunkCols;
+  while (cols < 4 * kChunkCols && w > 1.41421356 * cols) cols *= 2;  // nearest power of two
+  return std::min(qg, cols);
+}
 
 struct DevState {
   int dev = 0;
@@ -508,14 +531,14 @@ int copy_cols(double* dst, std::size_t lddst, const double* src, std::size_t lds
   return HMXG_OK;
 }
 
-// Host-pointer evaluation of columns [c0, c1) on device d: chunks of kChunkCols columns,
+// Host-pointer evaluation of columns [c0, c1) on device d: chunks of host_chunk_cols columns,
 // double-buffered staging, copies on their own streams so PCIe traffic in both
 // directions overlaps the kernels.
 int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size_t ldw, double* Y,
                        std::size_t ldy, std::size_t c0, std::size_t c1, bool time_phases, bool levels,
                        std::uint32_t* launches) {
   const std::size_t n = plan.n, qg = c1 - c0;
-  const std::size_t cq = std::min(qg, kChunkCols);
+  const std::size_t cq = host_chunk_cols(plan, qg);
   HMXG_TRY(ensure_workspace(plan, d, cq));
   HMXG_TRY(ensure_stage(plan, d, cq));
   const std::size_t chunks = (qg + cq - 1) / cq;
