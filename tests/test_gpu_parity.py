@@ -273,3 +273,28 @@ def test_strided_w_and_y(devices):
         assert np.all(yh[n:] == -7.0)
     ev.close()
     inst.close()
+
+
+def test_acceptance_criterion_3_on_the_gpu():
+    """Acceptance criterion 3 (proj/tests/acceptance.cpp:125-155) with the B200 evaluator:
+    50 reference-built instances (d cycling 2, 8, 32; n drawn in [256, 4096) or [256, 2048)
+    for d = 32; HSS and tau = 0.65 alternating; leaf 64, rank 32, budget 64, k-NN 8,
+    bacc 1e-3, seed 100 + i), W 3 columns, against the reference's evaluate_reference, for
+    several plans (schedule switches the evaluator accepts): worst relative error <= 1e-13."""
+    import random
+
+    rng = random.Random(33)
+    worst = 0.0
+    plans = [EvalPlan(), EvalPlan(block_lowering_near=True, block_lowering_far=True, coarsen_lowering=True, peel_top=True, p=4)]
+    for i in range(50):
+        d = (2, 8, 32)[i % 3]
+        n_max = 2048 if d == 32 else 4096
+        n = 256 + rng.randrange(n_max - 255)
+        spec = oracle.RefInstanceSpec(n=n, d=d, leaf=64, max_rank=32, budget=64, knn_k=8, bacc=1e-3, seed=100 + i,
+                                      mode=0 if i % 2 else 1, tau=0.65 if i % 2 else 0.0)
+        ri = oracle.RefInstance(spec)
+        w = oracle.random_matrix(n, 3, spec.seed)
+        ref = ri.evaluate_reference(w)
+        for plan in plans:
+            worst = max(worst, oracle.rel_frob(evaluate(ri.cds, plan, w), ref))
+    assert worst <= 1e-13, worst
