@@ -348,7 +348,10 @@ __device__ __forceinline__ void consume_chunks_pred(double (&acc)[4][4][2], std:
 // ---------------------------------------------------------------- tile bodies
 // Shared-memory carve-up of one CTA (both GEMM kernels): kStages x {A chunk, B tile}, the
 // stage barriers, a kTileRing-deep ring of claimed work items and their barriers.
-constexpr int kTileRing = 4;
+#ifndef HMXG_TILE_RING
+#define HMXG_TILE_RING 4
+#endif
+constexpr int kTileRing = HMXG_TILE_RING;
 // eval_dag: stored tiles travel from the consumer warps to the producer lane, which
 // publishes them at gpu scope (kSigRing-deep ring: counter address, 0 = nothing, kSigEnd)
 constexpr int kSigRing = 8;
