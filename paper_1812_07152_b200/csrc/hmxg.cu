@@ -13,6 +13,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -76,6 +77,10 @@ struct DevState {
   std::size_t stage_q = 0;  // host-path staging capacity (columns per buffer)
   double* w_stage[2] = {nullptr, nullptr};
   double* y_stage[2] = {nullptr, nullptr};
+  // pageable host W / Y (bounce path): pinned host staging of the same chunks
+  std::size_t pin_q = 0;
+  double* w_pin[2] = {nullptr, nullptr};
+  double* y_pin[2] = {nullptr, nullptr};
   std::uint64_t resident_bytes = 0;
   std::uint32_t* tile_counters = nullptr;  // one per GEMM launch, zeroed per evaluation
   // whole-evaluation DAG launch: work items (built per column count) and counters
@@ -135,12 +140,21 @@ struct DevState {
     }
     stage_q = 0;
   }
+  void release_pinned() {
+    for (int b = 0; b < 2; ++b) {
+      cudaFreeHost(w_pin[b]);
+      cudaFreeHost(y_pin[b]);
+      w_pin[b] = y_pin[b] = nullptr;
+    }
+    pin_q = 0;
+  }
   void release() {
     if (cudaSetDevice(dev) != cudaSuccess) return;
     for (cudaStream_t st : {comp, h2d, d2h})
       if (st) cudaStreamSynchronize(st);
     release_workspace();
     release_stage();
+    release_pinned();
     cudaFree(tiles);
     cudaFree(tile_counters);
     tile_counters = nullptr;
@@ -562,6 +576,88 @@ int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size
     HMXG_CUDA(cudaStreamWaitEvent(d.d2h, d.ev_done[b], 0));
     HMXG_TRY(copy_cols(Y + a * ldy, ldy, d.y_stage[b], n, n, m, cudaMemcpyDeviceToHost, d.d2h));
     HMXG_CUDA(cudaEventRecord(d.ev_out[b], d.d2h));
+  }
+  return HMXG_OK;
+}
+
+// Host memory the copy engines can read or write without staging (pinned or registered).
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Columns [c0, c0 + m) between a column-major host matrix and a contiguous n x m buffer,
+// split over `threads` host threads by column.
+void copy_columns_mt(double* dst, std::size_t lddst, const double* src, std::size_t ldsrc, std::size_t n,
+                     std::size_t m, unsigned threads) {
+  auto part = [&](std::size_t j0, std::size_t j1) {
+    for (std::size_t j = j0; j < j1; ++j) std::memcpy(dst + j * lddst, src + j * ldsrc, n * sizeof(double));
+  };
+  const std::size_t t = std::max<std::size_t>(1, std::min<std::size_t>(threads, m));
+  if (t == 1 || n * m * sizeof(double) < (std::size_t(1) << 22)) {
+    part(0, m);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (std::size_t k = 1; k < t; ++k) pool.emplace_back(part, m * k / t, m * (k + 1) / t);
+  part(0, m / t);
+  for (auto& th : pool) th.join();
+}
+
+// Host-pointer evaluation from pageable memory. cudaMemcpyAsync from pageable buffers is
+// staged by the driver and host-synchronous, so the chunk pipeline of enqueue_host_shard
+// collapses (cfg5-HSS: 615 ms per step against 90 ms from pinned buffers). Here the host
+// threads copy each chunk of W into pinned staging and each chunk of Y out of it, while the
+// copy engines and the evaluation work on the neighbouring chunks: chunk k+1 is staged and
+// chunk k-1 unstaged while chunk k is on the device. Returns when Y is complete.
+int host_bounce_shard(const Plan& plan, DevState& d, const double* W, std::size_t ldw, double* Y, std::size_t ldy,
+                      std::size_t c0, std::size_t c1, bool levels, std::uint32_t* launches, unsigned threads) {
+  HMXG_CUDA(cudaSetDevice(d.dev));
+  const std::size_t n = plan.n, qg = c1 - c0;
+  const std::size_t cq = host_chunk_cols(plan, qg);
+  HMXG_TRY(ensure_workspace(plan, d, cq));
+  HMXG_TRY(ensure_stage(plan, d, cq));
+  if (cq > d.pin_q) {
+    d.release_pinned();
+    for (int b = 0; b < 2; ++b) {
+      HMXG_CUDA(cudaHostAlloc(&d.w_pin[b], n * cq * sizeof(double), cudaHostAllocPortable));
+      HMXG_CUDA(cudaHostAlloc(&d.y_pin[b], n * cq * sizeof(double), cudaHostAllocPortable));
+    }
+    d.pin_q = cq;
+  }
+  const std::size_t chunks = (qg + cq - 1) / cq;
+  auto cols = [&](std::size_t k) { return std::min(cq, qg - k * cq); };
+  for (std::size_t k = 0; k <= chunks; ++k) {
+    if (k < chunks) {
+      const int b = static_cast<int>(k & 1);
+      const std::size_t a = c0 + k * cq, m = cols(k);
+      // pinned W buffer b is free once the H2D of chunk k-2 finished
+      if (k >= 2) HMXG_CUDA(cudaEventSynchronize(d.ev_in[b]));
+      copy_columns_mt(d.w_pin[b], n, W + a * ldw, ldw, n, m, threads);
+      if (k >= 2) HMXG_CUDA(cudaStreamWaitEvent(d.h2d, d.ev_done[b], 0));  // device W buffer b is free
+      HMXG_CUDA(cudaMemcpyAsync(d.w_stage[b], d.w_pin[b], n * m * sizeof(double), cudaMemcpyHostToDevice, d.h2d));
+      HMXG_CUDA(cudaEventRecord(d.ev_in[b], d.h2d));
+      HMXG_CUDA(cudaStreamWaitEvent(d.comp, d.ev_in[b], 0));
+      if (k >= 2) HMXG_CUDA(cudaStreamWaitEvent(d.comp, d.ev_out[b], 0));  // device Y buffer b is free
+      if (k == 0) HMXG_CUDA(cudaEventRecord(d.ev0, d.comp));
+      const DevState::DagItems* di = nullptr;
+      if (!levels) HMXG_TRY(ensure_dag(plan, d, m, d.comp, &di));
+      HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, false, levels, launches));
+      HMXG_CUDA(cudaEventRecord(d.ev_done[b], d.comp));
+      if (k + 1 == chunks) HMXG_CUDA(cudaEventRecord(d.ev1, d.comp));
+      HMXG_CUDA(cudaStreamWaitEvent(d.d2h, d.ev_done[b], 0));
+      HMXG_CUDA(cudaMemcpyAsync(d.y_pin[b], d.y_stage[b], n * m * sizeof(double), cudaMemcpyDeviceToHost, d.d2h));
+      HMXG_CUDA(cudaEventRecord(d.ev_out[b], d.d2h));
+    }
+    if (k >= 1) {  // chunk k-1 out of pinned Y buffer (k-1) & 1, which chunk k+1 reuses
+      const int b = static_cast<int>((k - 1) & 1);
+      HMXG_CUDA(cudaEventSynchronize(d.ev_out[b]));
+      copy_columns_mt(Y + (c0 + (k - 1) * cq) * ldy, ldy, d.y_pin[b], n, n, cols(k - 1), threads);
+    }
   }
   return HMXG_OK;
 }
@@ -1141,6 +1237,35 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     const std::size_t G = mat->devs.size();
     std::vector<std::size_t> cut(G + 1);
     for (std::size_t g = 0; g <= G; ++g) cut[g] = q * g / G;
+    if (!host_pinned(W) || !host_pinned(Y)) {
+      // pageable host buffers: the bounce path, one host thread per device shard
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const unsigned per = std::max(1u, hw / static_cast<unsigned>(G));
+      std::vector<int> rcs(G, HMXG_OK);
+      std::vector<std::string> errs(G);
+      std::vector<std::uint32_t> lc(G, 0);
+      auto run = [&](std::size_t g) {
+        rcs[g] = host_bounce_shard(plan, mat->devs[g], W, ldw, Y, ldy, cut[g], cut[g + 1], levels, &lc[g], per);
+        if (rcs[g] != HMXG_OK) errs[g] = hmxg_last_error();
+      };
+      std::vector<std::thread> workers;
+      for (std::size_t g = 1; g < G; ++g)
+        if (cut[g + 1] > cut[g]) workers.emplace_back(run, g);
+      if (cut[1] > cut[0]) run(0);
+      for (auto& th : workers) th.join();
+      for (std::size_t g = 0; g < G; ++g) {
+        if (rcs[g] != HMXG_OK) return set_err(rcs[g], errs[g]);
+        launches += lc[g];
+      }
+      for (std::size_t g = 0; g < G; ++g) {
+        if (cut[g + 1] == cut[g]) continue;
+        DevState& d = mat->devs[g];
+        HMXG_CUDA(cudaSetDevice(d.dev));
+        float ms = 0.f;
+        HMXG_CUDA(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
+        dev_ms = std::max(dev_ms, ms);
+      }
+    } else {
     for (std::size_t g = 0; g < G; ++g) {
       if (cut[g + 1] == cut[g]) continue;
       DevState& d = mat->devs[g];
@@ -1157,6 +1282,7 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       float ms = 0.f;
       HMXG_CUDA(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
       dev_ms = std::max(dev_ms, ms);
+    }
     }
   }
   if (stats) {
