@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <emmintrin.h>
+
 #include <algorithm>
 #include <cmath>
 #include <chrono>
@@ -594,8 +596,25 @@ bool host_pinned(const void* p) {
 // split over `threads` host threads by column.
 void copy_columns_mt(double* dst, std::size_t lddst, const double* src, std::size_t ldsrc, std::size_t n,
                      std::size_t m, unsigned threads) {
+  // Non-temporal stores: the destination (pinned staging read back by DMA, or the
+  // caller's Y) is not read by this thread, so no read-for-ownership traffic on it.
+  auto copy_col = [n](double* d, const double* s) {
+    std::size_t i = 0;
+    if ((reinterpret_cast<std::uintptr_t>(d) & 15) == 0) {
+      for (; i + 8 <= n; i += 8) {
+        const __m128d a = _mm_loadu_pd(s + i), b = _mm_loadu_pd(s + i + 2), c = _mm_loadu_pd(s + i + 4),
+                      e = _mm_loadu_pd(s + i + 6);
+        _mm_stream_pd(d + i, a);
+        _mm_stream_pd(d + i + 2, b);
+        _mm_stream_pd(d + i + 4, c);
+        _mm_stream_pd(d + i + 6, e);
+      }
+    }
+    for (; i < n; ++i) d[i] = s[i];
+  };
   auto part = [&](std::size_t j0, std::size_t j1) {
-    for (std::size_t j = j0; j < j1; ++j) std::memcpy(dst + j * lddst, src + j * ldsrc, n * sizeof(double));
+    for (std::size_t j = j0; j < j1; ++j) copy_col(dst + j * lddst, src + j * ldsrc);
+    _mm_sfence();
   };
   const std::size_t t = std::max<std::size_t>(1, std::min<std::size_t>(threads, m));
   if (t == 1 || n * m * sizeof(double) < (std::size_t(1) << 22)) {
