@@ -298,3 +298,30 @@ def test_acceptance_criterion_3_on_the_gpu():
         for plan in plans:
             worst = max(worst, oracle.rel_frob(evaluate(ri.cds, plan, w), ref))
     assert worst <= 1e-13, worst
+
+
+@pytest.mark.parametrize("devices", [(0,), (0, 0)])
+def test_pinned_and_pageable_host_paths_agree(devices):
+    """The host-pointer path runs the copy-engine pipeline on pinned buffers and the pinned
+    bounce path on pageable ones (numpy): the same bits, on one device and on two column
+    shards, and equal to the device-pointer path."""
+    import torch
+
+    spec, _ = config("cfg2-h2b")
+    inst = build_instance(spec)
+    n, q = inst.cds.n, 200
+    ev = Evaluator(inst.cds, devices=devices)
+    w = _w(n, q, 41)
+    y_pageable = ev.evaluate(w)
+    wh = torch.from_numpy(w.T.copy()).pin_memory()
+    yh = torch.empty_like(wh).pin_memory()
+    ev.evaluate_host_ptr(wh.data_ptr(), yh.data_ptr(), q)
+    assert np.array_equal(yh.numpy().T, y_pageable)
+    if len(devices) == 1:
+        wd = wh.cuda()
+        yd = torch.empty_like(wd)
+        ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, stream=torch_stream())
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy().T, y_pageable)
+    ev.close()
+    inst.close()
