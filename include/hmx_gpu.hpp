@@ -112,8 +112,10 @@ class Evaluator {
 };
 
 // hmx::evaluate(cds, plan, w, stats) on the GPU. The most recently used CDS stays
-// resident (keyed on object identity and generator storage), so repeated calls on the
-// same CDS upload it once.
+// resident, keyed on its content fingerprint (hmxg_cds_fingerprint: every structure array
+// and generator element, one multi-threaded host pass): an edited CDS, or a different one
+// at a reused address, is uploaded again, never evaluated from a stale copy. Callers that
+// evaluate one CDS many times and manage its lifetime hold an hmx_gpu::Evaluator instead.
 inline hmx::DenseMatrix evaluate(const hmx::CDS& cds, const hmx::EvalPlan& /*plan*/, const hmx::DenseMatrix& w,
                                  hmx::EvalStats* stats = nullptr) {
   if (w.rows != cds.tree.num_points())
@@ -123,23 +125,21 @@ inline hmx::DenseMatrix evaluate(const hmx::CDS& cds, const hmx::EvalPlan& /*pla
     return hmx::DenseMatrix(w.rows, 0);
   }
   struct Cached {
-    const hmx::CDS* cds = nullptr;
-    const double* dgen = nullptr;
-    const double* vgen = nullptr;
-    std::size_t sizes = 0;
+    std::uint64_t fingerprint = 0;
     std::unique_ptr<Evaluator> ev;
   };
   static std::mutex mu;
   static Cached cache;
   std::lock_guard<std::mutex> lock(mu);
-  const std::size_t sizes = cds.dgen.size() * 31 + cds.bgen.size() * 17 + cds.vgen.size();
-  if (cache.cds != &cds || cache.dgen != cds.dgen.data() || cache.vgen != cds.vgen.data() || cache.sizes != sizes) {
+  std::uint64_t fp = 0;
+  {
+    CdsView v(cds);
+    check(hmxg_cds_fingerprint(&v.view, &fp));
+  }
+  if (!cache.ev || cache.fingerprint != fp) {
     cache.ev.reset();
     cache.ev = std::make_unique<Evaluator>(cds);
-    cache.cds = &cds;
-    cache.dgen = cds.dgen.data();
-    cache.vgen = cds.vgen.data();
-    cache.sizes = sizes;
+    cache.fingerprint = fp;
   }
   return cache.ev->evaluate(w, stats);
 }

@@ -146,6 +146,12 @@ int hmxg_free(hmxg_mat* mat);
  * success, if info != NULL, the size fields (n, *_elems, skel_rows, launches_per_eval,
  * flops_per_col) are filled. */
 int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info);
+/* Content fingerprint of a view (host only, no device needed): a 64-bit hash of every
+ * structure array and every generator element, one multi-threaded pass at host memory
+ * bandwidth. The drop-in hmx_gpu::evaluate / Python evaluate() key their resident upload on
+ * it, so an edited or reallocated CDS is never evaluated from a stale upload (the reference
+ * evaluate, executor.cpp:274-302, reads the CDS on every call). */
+int hmxg_cds_fingerprint(const hmxg_cds_view* cds, uint64_t* out);
 /* Host-only check of the whole-evaluation DAG launch for q columns and a grid of `grid`
  * resident CTAs (no device needed): the claim order holds every task tile of the leaf
  * variant that runs exactly once, every tile an item waits for (B operand rows, identity

@@ -75,6 +75,7 @@ def _ref_lib():
             "hmxr_samples": (C.c_int, [vp, vp, vp]),
             "hmxr_basis": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(u64), vp, vp]),
             "hmxr_compress_seconds": (C.c_double, [vp]),
+            "hmxr_generate_plan": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32)]),
             "hmxr_mix64": (u64, [u64]),
             "hmxr_rng_fill_pm1": (None, [u64, u64, vp]),
             "hmxr_last_error": (C.c_char_p, []),
@@ -169,12 +170,22 @@ class RefInstance:
         self.cds = CDS.from_view(v, owner=self)
 
     def evaluate(self, w: np.ndarray, plan_bits: int = 0, p: int = 1) -> np.ndarray:
+        return self.evaluate_timed(w, plan_bits, p)[0]
+
+    def evaluate_timed(self, w: np.ndarray, plan_bits: int = 0, p: int = 1) -> tuple[np.ndarray, float]:
+        """hmx::evaluate and its EvalStats.seconds (executor.cpp:276,289-294)."""
         wf = np.asfortranarray(w, dtype=np.float64)
         y = np.zeros(wf.shape, dtype=np.float64, order="F")
         sec = C.c_double()
         _ref_check(_ref_lib().hmxr_evaluate(self._h, wf.ctypes.data_as(C.c_void_p), wf.shape[0], wf.shape[1],
                                             y.ctypes.data_as(C.c_void_p), plan_bits, p, C.byref(sec)))
-        return y
+        return y, sec.value
+
+    def generate_plan(self, p: int) -> int:
+        """hmx::generate_plan on the instance's tree, blocks and coarsening (lowering bits)."""
+        bits = C.c_uint32()
+        _ref_check(_ref_lib().hmxr_generate_plan(self._h, p, C.byref(bits)))
+        return int(bits.value)
 
     def evaluate_reference(self, w: np.ndarray) -> np.ndarray:
         wf = np.asfortranarray(w, dtype=np.float64)

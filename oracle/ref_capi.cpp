@@ -449,6 +449,19 @@ int hmxr_basis(void* inst, std::uint32_t node, std::uint32_t* srank, std::uint64
 
 double hmxr_compress_seconds(void* inst) { return static_cast<RefInstance*>(inst)->compress_seconds; }
 
+// hmx::generate_plan (executor.cpp:259-272) over the instance's own tree, blocks and
+// coarsening with p workers: the stock plan, as lowering bits for hmxr_evaluate.
+int hmxr_generate_plan(void* inst, std::uint32_t p, std::uint32_t* bits) {
+  auto* in = static_cast<RefInstance*>(inst);
+  return guarded([&] {
+    hmx::PlanDefaults d;
+    d.p = p;
+    const hmx::EvalPlan plan = hmx::generate_plan(in->ht.tree, in->nbs, in->fbs, in->cs, d);
+    *bits = (plan.block_lowering_near ? 1u : 0u) | (plan.block_lowering_far ? 2u : 0u) |
+            (plan.coarsen_lowering ? 4u : 0u) | (plan.peel_top ? 8u : 0u);
+  });
+}
+
 // The reference RNG primitives, so the CLI's random W (hmx.cpp:117-122) can be pinned.
 std::uint64_t hmxr_mix64(std::uint64_t x) { return hmx::mix64(x); }
 

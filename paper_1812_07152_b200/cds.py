@@ -46,6 +46,16 @@ class CDS:
     owner: Any = None  # keeps a native producer alive when arrays are zero-copy views
     _cache: dict = field(default_factory=dict, repr=False)
 
+    def fingerprint(self) -> int:
+        """Content hash of every array (``hmxg_cds_fingerprint``): equal only for equal CDSs,
+        up to 64-bit hash collisions. One multi-threaded pass over the generators."""
+        out = C.c_uint64()
+        v = self.view()
+        rc = N.hmxg().hmxg_cds_fingerprint(C.byref(v), C.byref(out))
+        if rc:
+            raise ValueError(N.last_error(N.hmxg(), "hmxg"))
+        return int(out.value)
+
     # ---- reference accessors (structure.hpp:104-128)
     def is_leaf(self, i: int) -> bool:
         return int(self.lchild[i]) == N.HMXG_NO_NODE

@@ -99,6 +99,10 @@ struct DevState {
   std::uint32_t* node_tiles = nullptr;
   std::uint32_t* yp_tiles = nullptr;
   std::uint32_t* remote_t = nullptr;  // split mode: nodes whose T comes from the exchange
+  // HMXG_POISON=1 (debug): live T/S rows, NaN-filled with Wp and Yp before every evaluation
+  bool poison = false;
+  std::uint32_t* ts_live = nullptr;
+  std::uint64_t ts_live_count = 0;
   // CUDA graph of the whole launch sequence for one (W, Y, q, ld, stream, workspace) key:
   // repeated device-pointer evaluations replay it instead of issuing ~2H+4 launches.
   struct GraphKey {
@@ -107,14 +111,21 @@ struct DevState {
     std::size_t q = 0, ldw = 0, ldy = 0;
     cudaStream_t st = nullptr;
     const double* wp = nullptr;
+    const std::uint64_t* items = nullptr;  // the DAG item list and counters the graph reads
+    const std::uint32_t* dag_done = nullptr;
     bool levels = false;
     bool timed = false;  // captured with per-launch event nodes (and without programmatic launch)
     bool operator==(const GraphKey& o) const {
       return w == o.w && y == o.y && q == o.q && ldw == o.ldw && ldy == o.ldy && st == o.st && wp == o.wp &&
-             levels == o.levels && timed == o.timed;
+             items == o.items && dag_done == o.dag_done && levels == o.levels && timed == o.timed;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
+  // Ordering between calls: every call shares the workspace (Wp, T, S, Yp, the DAG counters).
+  // A device-pointer call may return before its work is done (HMXG_F_NO_SYNC); ev_last marks
+  // the end of its work on its stream, and the next call, on whatever stream, waits for it.
+  cudaEvent_t ev_last = nullptr;
+  bool pending = false;
   bool last_levels = false;  // launch sequence of the last evaluation (phase reporting)
   std::size_t last_q = 0;    // its column count (per device shard)
   std::uint32_t glaunches = 0;
@@ -170,6 +181,8 @@ struct DevState {
     yp_tiles = nullptr;
     cudaFree(remote_t);
     remote_t = nullptr;
+    cudaFree(ts_live);
+    ts_live = nullptr;
     dag_done = nullptr;
     dag_done_cap = 0;
     node_tiles = nullptr;
@@ -182,7 +195,7 @@ struct DevState {
     tasks = nullptr;
     segs = nullptr;
     ipmap = nullptr;
-    for (cudaEvent_t* e : {&ev0, &ev1, &ev_in[0], &ev_in[1], &ev_done[0], &ev_done[1], &ev_out[0], &ev_out[1]})
+    for (cudaEvent_t* e : {&ev0, &ev1, &ev_in[0], &ev_in[1], &ev_done[0], &ev_done[1], &ev_out[0], &ev_out[1], &ev_last})
       if (*e) cudaEventDestroy(*e), *e = nullptr;
     for (auto& e : phase_ev) cudaEventDestroy(e);
     phase_ev.clear();
@@ -209,6 +222,8 @@ namespace {
 int ensure_workspace(const Plan& plan, DevState& d, std::size_t q) {
   q = phys_cols(q);
   if (q <= d.cap_q) return HMXG_OK;
+  HMXG_CUDA(cudaDeviceSynchronize());  // an earlier asynchronous call may still use the buffers
+  d.pending = false;
   d.release_workspace();
   const std::size_t n = plan.rows_pad, r = plan.skel_rows;
   HMXG_CUDA(cudaMalloc(&d.wp, n * q * sizeof(double)));
@@ -334,7 +349,11 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
       return HMXG_OK;
     }
   DevState::DagItems& e = d.dag[d.dag_next++ % 4];
-  HMXG_CUDA(cudaStreamSynchronize(st));  // the slot's previous list may still be in use
+  // the slot's previous list may still be in use (this stream, or an earlier asynchronous
+  // call on another one), and the cached graph may have captured it
+  HMXG_CUDA(cudaStreamSynchronize(st));
+  if (d.pending) HMXG_CUDA(cudaEventSynchronize(d.ev_last));
+  if (e.items) d.drop_graph();
   cudaFree(e.items);
   e = DevState::DagItems{};
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage, d.gemm_grid);
@@ -342,6 +361,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
   const std::size_t words = dag_done_words(plan, q);
   if (words > d.dag_done_cap) {
+    d.drop_graph();
     cudaFree(d.dag_done);
     d.dag_done = nullptr;
     HMXG_CUDA(cudaMalloc(&d.dag_done, words * sizeof(std::uint32_t)));
@@ -449,6 +469,16 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   };
   CUtensorMap tm_wp, tm_t, tm_s;
   const std::uint64_t ldq = d.cap_q;
+  if (d.poison) {  // debug race detector: every live workspace row NaN before the launches
+    const std::uint64_t pc = phys_cols(q);
+    poison_rows<<<1184, 256, 0, st>>>(d.wp, ldq, d.ipmap, plan.n, pc);
+    poison_rows<<<1184, 256, 0, st>>>(d.yp, ldq, d.ipmap, plan.n, pc);
+    if (d.ts_live_count) {
+      poison_rows<<<1184, 256, 0, st>>>(d.t, ldq, d.ts_live, d.ts_live_count, pc);
+      poison_rows<<<1184, 256, 0, st>>>(d.s, ldq, d.ts_live, d.ts_live_count, pc);
+    }
+    HMXG_CUDA(cudaGetLastError());
+  }
   HMXG_TRY(make_map(&tm_wp, d.wp, plan.rows_pad, q, ldq));
   HMXG_TRY(make_map(&tm_t, d.t, plan.skel_rows, q, ldq));
   HMXG_TRY(make_map(&tm_s, d.s, plan.skel_rows, q, ldq));
@@ -582,14 +612,29 @@ int enqueue_host_shard(const Plan& plan, DevState& d, const double* W, std::size
   return HMXG_OK;
 }
 
-// Host memory the copy engines can read or write without staging (pinned or registered).
-bool host_pinned(const void* p) {
+// What a W / Y pointer of the host path is: memory the copy engines can read or write
+// without staging (pinned or registered), pageable (or managed: staged by the host threads
+// like pageable memory), or device memory, which needs HMXG_F_DEVICE_PTRS.
+enum class HostKind { kPageable, kPinned, kDevice };
+HostKind host_kind(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return HostKind::kPageable;
   }
-  return a.type == cudaMemoryTypeHost;
+  if (a.type == cudaMemoryTypeDevice) return HostKind::kDevice;
+  return a.type == cudaMemoryTypeHost ? HostKind::kPinned : HostKind::kPageable;
+}
+
+// The stream `st` of device d waits for the previous call's work (see DevState::ev_last).
+// Not inside a capture the caller runs: its graph cannot wait on an event recorded outside.
+int order_after_previous(DevState& d, cudaStream_t st) {
+  if (!d.pending) return HMXG_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HMXG_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return HMXG_OK;
+  HMXG_CUDA(cudaStreamWaitEvent(st, d.ev_last, 0));
+  return HMXG_OK;
 }
 
 // Columns [c0, c0 + m) between a column-major host matrix and a contiguous n x m buffer,
@@ -634,7 +679,8 @@ void copy_columns_mt(double* dst, std::size_t lddst, const double* src, std::siz
 // copy engines and the evaluation work on the neighbouring chunks: chunk k+1 is staged and
 // chunk k-1 unstaged while chunk k is on the device. Returns when Y is complete.
 int host_bounce_shard(const Plan& plan, DevState& d, const double* W, std::size_t ldw, double* Y, std::size_t ldy,
-                      std::size_t c0, std::size_t c1, bool levels, std::uint32_t* launches, unsigned threads) {
+                      std::size_t c0, std::size_t c1, bool time_phases, bool levels, std::uint32_t* launches,
+                      unsigned threads) {
   HMXG_CUDA(cudaSetDevice(d.dev));
   const std::size_t n = plan.n, qg = c1 - c0;
   const std::size_t cq = host_chunk_cols(plan, qg);
@@ -665,7 +711,8 @@ int host_bounce_shard(const Plan& plan, DevState& d, const double* W, std::size_
       if (k == 0) HMXG_CUDA(cudaEventRecord(d.ev0, d.comp));
       const DevState::DagItems* di = nullptr;
       if (!levels) HMXG_TRY(ensure_dag(plan, d, m, d.comp, &di));
-      HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, false, levels, launches));
+      HMXG_TRY(enqueue_eval(plan, d, d.w_stage[b], n, d.y_stage[b], n, m, d.comp, time_phases && k == 0, levels,
+                            launches));
       HMXG_CUDA(cudaEventRecord(d.ev_done[b], d.comp));
       if (k + 1 == chunks) HMXG_CUDA(cudaEventRecord(d.ev1, d.comp));
       HMXG_CUDA(cudaStreamWaitEvent(d.d2h, d.ev_done[b], 0));
@@ -789,6 +836,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
         HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    HMXG_CUDA(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
     d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -843,6 +891,18 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.yp_tiles, plan.yp_tiles.data(), plan.yp_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
+    {
+      const char* pz = std::getenv("HMXG_POISON");
+      d.poison = split.nparts == 1 && pz && *pz && std::strcmp(pz, "0") != 0;
+      if (d.poison) {
+        std::vector<std::uint32_t> live;
+        for (std::uint32_t i = 0; i < plan.num_nodes; ++i)
+          if (cds->participating[i] && cds->sranks[i] > 0)
+            for (std::uint32_t r = 0; r < cds->sranks[i]; ++r) live.push_back(static_cast<std::uint32_t>(plan.node_off[i] + r));
+        HMXG_TRY(dev_upload(&d.ts_live, live.data(), live.size(), d.comp));
+        d.ts_live_count = live.size();
+      }
+    }
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
     d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
                        4 * plan.ipmap.size() + 4 * plan.idmap.size();
@@ -889,6 +949,86 @@ int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
 
 int hmxg_destroy(hmxg_ctx* ctx) {
   delete ctx;
+  return HMXG_OK;
+}
+
+}  // extern "C"
+
+namespace hmxg {
+namespace {
+// Content fingerprint of a CDS view (hmxg_cds_fingerprint): xxHash64-style rounds (four
+// 64-bit lanes, multiply-rotate-multiply, then an avalanche) over every array, 4 MiB blocks
+// hashed in parallel and combined in order. One pass over the CDS at host memory bandwidth.
+constexpr std::uint64_t kP1 = 0x9E3779B185EBCA87ull, kP2 = 0xC2B2AE3D27D4EB4Full, kP3 = 0x165667B19E3779F9ull,
+                        kP4 = 0x85EBCA77C2B2AE63ull, kP5 = 0x27D4EB2F165667C5ull;
+inline std::uint64_t rotl64(std::uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+inline std::uint64_t fp_round(std::uint64_t acc, std::uint64_t in) { return rotl64(acc + in * kP2, 31) * kP1; }
+inline std::uint64_t fp_avalanche(std::uint64_t h) {
+  h ^= h >> 33;
+  h *= kP2;
+  h ^= h >> 29;
+  h *= kP3;
+  return h ^ (h >> 32);
+}
+std::uint64_t fp_block(const unsigned char* p, std::size_t len, std::uint64_t seed) {
+  std::uint64_t a[4] = {seed + kP1 + kP2, seed + kP2, seed, seed - kP1};
+  std::size_t i = 0;
+  for (; i + 32 <= len; i += 32)
+    for (int l = 0; l < 4; ++l) {
+      std::uint64_t w;
+      std::memcpy(&w, p + i + 8 * l, 8);  // generators inside a mapped file need not be aligned
+      a[l] = fp_round(a[l], w);
+    }
+  std::uint64_t h = rotl64(a[0], 1) + rotl64(a[1], 7) + rotl64(a[2], 12) + rotl64(a[3], 18) + len;
+  for (; i < len; ++i) h = rotl64(h ^ (p[i] * kP5), 11) * kP1;
+  return fp_avalanche(h);
+}
+std::uint64_t fp_array(const void* data, std::size_t bytes, std::uint64_t h) {
+  constexpr std::size_t kBlock = std::size_t(4) << 20;
+  const auto* p = static_cast<const unsigned char*>(data);
+  const std::size_t nb = (bytes + kBlock - 1) / kBlock;
+  std::vector<std::uint64_t> bh(nb);
+  auto work = [&](std::size_t b0, std::size_t b1) {
+    for (std::size_t b = b0; b < b1; ++b) bh[b] = fp_block(p + b * kBlock, std::min(kBlock, bytes - b * kBlock), b);
+  };
+  const std::size_t t = std::min<std::size_t>(std::max(1u, std::thread::hardware_concurrency()), nb);
+  if (t <= 1) {
+    work(0, nb);
+  } else {
+    std::vector<std::thread> pool;
+    for (std::size_t k = 1; k < t; ++k) pool.emplace_back(work, nb * k / t, nb * (k + 1) / t);
+    work(0, nb / t);
+    for (auto& th : pool) th.join();
+  }
+  h = fp_round(h, bytes);
+  for (std::uint64_t x : bh) h = fp_round(h ^ x, kP4);
+  return h;
+}
+}  // namespace
+}  // namespace hmxg
+
+extern "C" {
+
+int hmxg_cds_fingerprint(const hmxg_cds_view* v, uint64_t* out) {
+  if (!v || !out) return set_err(HMXG_EINVAL, "hmxg_cds_fingerprint: null argument");
+  const std::size_t nn = v->num_nodes, n = v->n;
+  std::uint64_t h = fp_round(fp_round(kP5, n), (std::uint64_t(v->height) << 32) | nn);
+  auto arr = [&](const void* p, std::size_t bytes) {
+    if (bytes && !p) return false;
+    h = fp_array(p, bytes, h);
+    return true;
+  };
+  bool ok = arr(v->parent, 4 * nn) && arr(v->lchild, 4 * nn) && arr(v->rchild, 4 * nn) && arr(v->start, 4 * nn) &&
+            arr(v->end, 4 * nn) && arr(v->level, 4 * nn) && arr(v->perm, 4 * n) && arr(v->sranks, 4 * nn) &&
+            arr(v->participating, nn) && arr(v->near_pairs, 8 * v->num_near) && arr(v->far_pairs, 8 * v->num_far) &&
+            arr(v->v_order, 4 * v->num_v) && arr(v->dptr, 8 * (v->num_near + 1)) &&
+            arr(v->bptr, 8 * (v->num_far + 1)) && arr(v->vptr, 8 * (v->num_v + 1));
+  if (!ok) return set_err(HMXG_EINVAL, "cds: null array in view");
+  // generator extents come from the offset arrays (the view was checked to hold them above)
+  ok = arr(v->dgen, 8 * v->dptr[v->num_near]) && arr(v->bgen, 8 * v->bptr[v->num_far]) &&
+       arr(v->vgen, 8 * v->vptr[v->num_v]);
+  if (!ok) return set_err(HMXG_EINVAL, "cds: null generator in view");
+  *out = fp_avalanche(h);
   return HMXG_OK;
 }
 
@@ -1035,6 +1175,8 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   HMXG_TRY(ensure_workspace(plan, d, q));
   const DevState::DagItems* di = nullptr;
   HMXG_TRY(ensure_dag(plan, d, q, st, &di, static_cast<std::uint32_t>(stage)));
+  HMXG_TRY(order_after_previous(d, st));
+  d.pending = false;  // this call returns when its stage (and everything before it) is done
   const std::uint32_t qq = static_cast<std::uint32_t>(q), nn = static_cast<std::uint32_t>(n);
   const std::uint64_t ldq = d.cap_q;
   const std::uint32_t ncb = (qq + kBN - 1) / kBN;
@@ -1202,7 +1344,10 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
   const Plan& plan = mat->plan;
   const bool time_phases = flags & HMXG_F_TIME_PHASES;
   const bool levels = flags & HMXG_F_LEVEL_LAUNCHES;
-  for (auto& dv : mat->devs) dv.last_levels = levels;
+  for (auto& dv : mat->devs) {
+    dv.last_levels = levels;
+    dv.phase_valid = false;  // set again by the launches of this call if they are timed
+  }
   std::uint32_t launches = 0;
   float dev_ms = 0.f;
 
@@ -1214,14 +1359,16 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.comp;
     HMXG_TRY(ensure_workspace(plan, d, q));
     const DevState::DagItems* di = nullptr;
-    if (!levels) HMXG_TRY(ensure_dag(plan, d, q, st ? st : d.comp, &di));
+    if (!levels) HMXG_TRY(ensure_dag(plan, d, q, st, &di));
+    HMXG_TRY(order_after_previous(d, st));
     const bool sync = !(flags & HMXG_F_NO_SYNC);
     if (sync) HMXG_CUDA(cudaEventRecord(d.ev0, st));
     // the legacy / per-thread default streams cannot be captured: launch directly there
     if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread || (flags & HMXG_F_NO_GRAPH)) {
       HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &launches));
     } else {
-      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, levels, time_phases};
+      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, di ? di->items : nullptr, d.dag_done, levels,
+                                   time_phases};
       if (!(d.gexec && d.gkey == key)) {
         d.drop_graph();
         cudaGraph_t graph = nullptr;
@@ -1247,16 +1394,34 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       HMXG_CUDA(cudaEventRecord(d.ev1, st));
       HMXG_CUDA(cudaEventSynchronize(d.ev1));
       HMXG_CUDA(cudaEventElapsedTime(&dev_ms, d.ev0, d.ev1));
+      d.pending = false;
 #ifdef HMXG_TRACE
       if (!levels) trace_dump(plan, q, d.gemm_grid);
 #endif
+    } else {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      HMXG_CUDA(cudaStreamIsCapturing(st, &cap));
+      if (cap == cudaStreamCaptureStatusNone) {  // the next call waits for this one's work
+        HMXG_CUDA(cudaEventRecord(d.ev_last, st));
+        d.pending = true;
+      }
     }
   } else {
     // column sharding over the context's devices: Y[:,c] depends only on W[:,c]
+    const HostKind kw = host_kind(W), ky = host_kind(Y);
+    if (kw == HostKind::kDevice || ky == HostKind::kDevice)
+      return set_err(HMXG_EINVAL, "hmxg_evaluate: device pointer without HMXG_F_DEVICE_PTRS");
     const std::size_t G = mat->devs.size();
     std::vector<std::size_t> cut(G + 1);
     for (std::size_t g = 0; g <= G; ++g) cut[g] = q * g / G;
-    if (!host_pinned(W) || !host_pinned(Y)) {
+    for (std::size_t g = 0; g < G; ++g) {  // an earlier asynchronous device-pointer call
+      DevState& d = mat->devs[g];
+      if (!d.pending) continue;
+      HMXG_CUDA(cudaSetDevice(d.dev));
+      HMXG_CUDA(cudaEventSynchronize(d.ev_last));
+      d.pending = false;
+    }
+    if (kw != HostKind::kPinned || ky != HostKind::kPinned) {
       // pageable host buffers: the bounce path, one host thread per device shard
       const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
       const unsigned per = std::max(1u, hw / static_cast<unsigned>(G));
@@ -1264,7 +1429,8 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       std::vector<std::string> errs(G);
       std::vector<std::uint32_t> lc(G, 0);
       auto run = [&](std::size_t g) {
-        rcs[g] = host_bounce_shard(plan, mat->devs[g], W, ldw, Y, ldy, cut[g], cut[g + 1], levels, &lc[g], per);
+        rcs[g] = host_bounce_shard(plan, mat->devs[g], W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0,
+                                   levels, &lc[g], per);
         if (rcs[g] != HMXG_OK) errs[g] = hmxg_last_error();
       };
       std::vector<std::thread> workers;
@@ -1276,21 +1442,14 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
         if (rcs[g] != HMXG_OK) return set_err(rcs[g], errs[g]);
         launches += lc[g];
       }
+    } else {
       for (std::size_t g = 0; g < G; ++g) {
         if (cut[g + 1] == cut[g]) continue;
         DevState& d = mat->devs[g];
         HMXG_CUDA(cudaSetDevice(d.dev));
-        float ms = 0.f;
-        HMXG_CUDA(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
-        dev_ms = std::max(dev_ms, ms);
+        HMXG_TRY(enqueue_host_shard(plan, d, W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0, levels,
+                                    &launches));
       }
-    } else {
-    for (std::size_t g = 0; g < G; ++g) {
-      if (cut[g + 1] == cut[g]) continue;
-      DevState& d = mat->devs[g];
-      HMXG_CUDA(cudaSetDevice(d.dev));
-      HMXG_TRY(enqueue_host_shard(plan, d, W, ldw, Y, ldy, cut[g], cut[g + 1], time_phases && g == 0, levels,
-                                  &launches));
     }
     for (std::size_t g = 0; g < G; ++g) {
       if (cut[g + 1] == cut[g]) continue;
@@ -1298,10 +1457,10 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
       HMXG_CUDA(cudaSetDevice(d.dev));
       HMXG_CUDA(cudaStreamSynchronize(d.d2h));
       HMXG_CUDA(cudaStreamSynchronize(d.comp));
+      HMXG_CUDA(cudaEventSynchronize(d.ev1));
       float ms = 0.f;
       HMXG_CUDA(cudaEventElapsedTime(&ms, d.ev0, d.ev1));
       dev_ms = std::max(dev_ms, ms);
-    }
     }
   }
   if (stats) {

@@ -927,6 +927,21 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   }
 }
 
+// Race detector of debug runs (HMXG_POISON=1): every live row of a workspace buffer (the
+// rows of `rows`, all physical columns of the call) is set to NaN before the evaluation, so a
+// tile read before its producer stored it (or a row nobody writes) surfaces as NaN in Y
+// instead of as the previous evaluation's data. Pad rows stay zero: the 16-row B chunks read
+// them as zeros by design.
+__global__ void __launch_bounds__(256) poison_rows(double* __restrict__ buf, std::uint64_t ld,
+                                                   const std::uint32_t* __restrict__ rows, std::uint64_t nrows,
+                                                   std::uint64_t ncols) {
+  const double nan = __longlong_as_double(0x7ff8dead00000000ll);
+  const std::uint64_t total = nrows * ncols;
+  for (std::uint64_t e = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    buf[static_cast<std::uint64_t>(rows[e / ncols]) * ld + e % ncols] = nan;
+}
+
 // Subtree-split stage 1: the T tiles of the other parts' nodes were filled by the
 // exchange; mark them complete for every column block.
 __global__ void preset_done(const std::uint32_t* __restrict__ nodes, std::uint32_t count, std::uint32_t* done_t,

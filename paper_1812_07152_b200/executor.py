@@ -261,11 +261,19 @@ class Evaluator:
 
 
 def _evaluator_for(cds: CDS, devices=(0,)) -> Evaluator:
+    """The resident upload of ``cds`` for the drop-in ``evaluate``, keyed on the CDS's content
+    fingerprint: an in-place edit of any array (or a different CDS at the same address)
+    uploads again instead of evaluating a stale copy. The reference's evaluate has no cache
+    (executor.cpp:274-302); the fingerprint pass costs one read of the CDS on the host."""
     key = ("evaluator", tuple(devices))
-    ev = cds._cache.get(key)
-    if ev is None:
-        ev = Evaluator(cds, devices)
-        cds._cache[key] = ev
+    fp = cds.fingerprint()
+    hit = cds._cache.get(key)
+    if hit is not None and hit[0] == fp:
+        return hit[1]
+    if hit is not None:
+        hit[1].close()
+    ev = Evaluator(cds, devices)
+    cds._cache[key] = (fp, ev)
     return ev
 
 
@@ -273,7 +281,8 @@ def evaluate(cds: CDS, plan: EvalPlan | None, w: np.ndarray, stats: EvalStats | 
              devices=(0,)) -> np.ndarray:
     """``hmx::evaluate(cds, plan, w, &stats)`` on the B200 (executor.cpp:274-302).
 
-    The CDS is uploaded on first use and stays resident (cached on the CDS object).
+    The CDS is uploaded on first use and stays resident (cached on the CDS object, keyed on
+    its content fingerprint, so edits are seen). ``Evaluator`` is the explicit handle.
     """
     if w.ndim != 2 or w.shape[0] != cds.n:
         raise ValueError("evaluate: W row count does not match the point count")

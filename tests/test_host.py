@@ -266,3 +266,25 @@ def test_dag_claim_order_baseline_configs(name):
     for qq in (q, 4 * q):
         assert N.hmxg().hmxg_dag_check(C.byref(v), qq, 444, None) == 0, N.last_error(N.hmxg(), "hmxg")
     inst.close()
+
+
+def test_cds_fingerprint_sees_every_edit():
+    """hmxg_cds_fingerprint (the drop-in caches' key): stable across calls and copies, and
+    changed by a one-ulp edit of any generator, a structure edit, or a different CDS."""
+    inst = _small()
+    cds = inst.cds
+    fp = cds.fingerprint()
+    assert fp == cds.fingerprint()
+    for name in ("dgen", "bgen", "vgen"):
+        arr = getattr(cds, name)
+        k = arr.size // 2
+        old = arr[k]
+        arr[k] = np.nextafter(old, np.inf)
+        assert cds.fingerprint() != fp, name
+        arr[k] = old
+        assert cds.fingerprint() == fp
+    cds.perm[[0, 1]] = cds.perm[[1, 0]]
+    assert cds.fingerprint() != fp
+    cds.perm[[0, 1]] = cds.perm[[1, 0]]
+    other = build_instance(InstanceSpec(n=1500, d=3, leaf=40, max_rank=24, mode="budget", budget=0.1, h=0.4, seed=3))
+    assert other.cds.fingerprint() != fp
