@@ -98,6 +98,14 @@ struct DevState {
   std::size_t dag_done_cap = 0;
   std::uint32_t* node_tiles = nullptr;
   std::uint32_t* yp_tiles = nullptr;
+  // fused permutations (small problems, see fused_io): padded row -> point, and the leaf jobs
+  std::uint32_t* pmap = nullptr;
+  uint4* leaf_jobs = nullptr;
+  std::uint32_t njobs = 0;
+  // an enqueue failed between eval_dag and the launch that zeroes its counters: zero them first
+  bool counters_dirty = false;
+  bool last_fused = false;  // the last evaluation ran the single fused launch
+  std::uint32_t last_launches = 3;
   std::uint32_t* remote_t = nullptr;  // split mode: nodes whose T comes from the exchange
   // HMXG_POISON=1 (debug): live T/S rows, NaN-filled with Wp and Yp before every evaluation
   bool poison = false;
@@ -129,6 +137,7 @@ struct DevState {
   bool last_levels = false;  // launch sequence of the last evaluation (phase reporting)
   std::size_t last_q = 0;    // its column count (per device shard)
   std::uint32_t glaunches = 0;
+  bool gfused = false;  // the cached graph is the fused single launch
   unsigned gemm_grid = 0;                   // resident CTAs of the persistent GEMM
 
   void drop_graph() {
@@ -183,6 +192,10 @@ struct DevState {
     remote_t = nullptr;
     cudaFree(ts_live);
     ts_live = nullptr;
+    cudaFree(pmap);
+    pmap = nullptr;
+    cudaFree(leaf_jobs);
+    leaf_jobs = nullptr;
     dag_done = nullptr;
     dag_done_cap = 0;
     node_tiles = nullptr;
@@ -333,11 +346,23 @@ std::uint32_t forward_signals(std::uint32_t nitems, unsigned grid) {
   return nitems >= std::uint64_t(HMXG_FWD_MIN_ITEMS_PER_CTA) * grid ? 1u : 0u;
 }
 
-// [claim counter per stage | T counters | S counters | Yp counters] (nodes x ncb each)
+// [claim counter per stage | T counters | S counters | Yp counters | Wp counters] (nodes x ncb
+// each), then the exit counter of the launch's self-reset (DagParams::reset_words)
 constexpr std::size_t kDagClaimWords = 2;
 std::size_t dag_done_words(const Plan& plan, std::size_t q) {
   const std::size_t ncb = (q + kBN - 1) / kBN;
-  return kDagClaimWords + 3 * std::size_t(plan.num_nodes) * ncb;  // T, S, Yp counters
+  return kDagClaimWords + 4 * std::size_t(plan.num_nodes) * ncb;  // T, S, Yp, Wp counters
+}
+
+// Small problems run the permutations inside the DAG launch (DagParams::fused): one launch,
+// Wp gathered per (leaf, column block) by the CTAs before their first item, final leaf rows
+// stored straight into Y. For large W the dedicated transpose kernels move the data at HBM
+// speed and the DAG keeps all of its issue slots for the DMMAs.
+#ifndef HMXG_FUSED_MAX_ELEMS
+#define HMXG_FUSED_MAX_ELEMS (1u << 22)
+#endif
+bool fused_io(const Plan& plan, std::size_t q) {
+  return plan.nparts == 1 && plan.n * q <= std::uint64_t(HMXG_FUSED_MAX_ELEMS) && std::getenv("HMXG_NO_FUSED") == nullptr;
 }
 
 // Item list and counters for q columns (built on first use, cached for a few q).
@@ -364,8 +389,12 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
     d.drop_graph();
     cudaFree(d.dag_done);
     d.dag_done = nullptr;
-    HMXG_CUDA(cudaMalloc(&d.dag_done, words * sizeof(std::uint32_t)));
+    HMXG_CUDA(cudaMalloc(&d.dag_done, (words + 1) * sizeof(std::uint32_t)));
+    // every launch leaves the counters zero for the next one (permute_out or the DAG's own
+    // last CTA zeroes them); a new buffer starts zero
+    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, (words + 1) * sizeof(std::uint32_t), st));
     d.dag_done_cap = words;
+    d.counters_dirty = false;
   }
   HMXG_CUDA(cudaStreamSynchronize(st));
   e.nitems = static_cast<std::uint32_t>(items.size());
@@ -500,6 +529,9 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     for (const auto& e : d.dag)
       if (e.items && e.q == q && e.stage == 0) di = &e;
     if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
+    const std::size_t words = dag_done_words(plan, q);
+    const bool fused = fused_io(plan, q);
+    d.last_fused = fused;
     DagParams dp{};
     dp.items = di->items;
     dp.nitems = di->nitems;
@@ -516,28 +548,58 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     HMXG_TRY(trace_prepare(d, st));
     dp.trace = g_trace;
 #endif
+    if (d.counters_dirty) HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, (words + 1) * sizeof(std::uint32_t), st));
+    d.counters_dirty = true;  // until the launch that zeroes them is enqueued
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
+    if (fused) {
+      // one launch: permutations inside, counters zeroed by the DAG's last CTA
+      dp.fused = 1;
+      dp.njobs = d.njobs;
+      dp.leaf_jobs = d.leaf_jobs;
+      dp.w = w;
+      dp.ldw = ldw;
+      dp.pmap = d.pmap;
+      dp.reset_words = static_cast<std::uint32_t>(words);
+      dp.exit_ctr = d.dag_done + words;
+      p.y_final = y;
+      p.ldy = ldy;
+      p.pmap = d.pmap;
+      const unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, d.njobs * dp.ncb));
+      HMXG_TRY(mark());
+      eval_dag<<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+      ++*launches;
+      HMXG_TRY(mark());
+      HMXG_CUDA(cudaGetLastError());
+      d.counters_dirty = false;
+      d.last_launches = 1;
+      if (time_phases) d.phase_valid = true;
+      return HMXG_OK;
+    }
     HMXG_TRY(mark());
     const dim3 pgrid2((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
     if (pgrid2.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
-    // permute_in also zeroes the DAG's counters; eval_dag and permute_out are programmatic
-    // dependent launches (their launch overlaps the predecessor; they wait in-kernel). With
-    // per-launch timing the dependents launch normally, so each event brackets one kernel.
-    permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, d.dag_done, dag_done_words(plan, q));
+    // eval_dag and permute_out are programmatic dependent launches (their launch overlaps the
+    // predecessor; they wait in-kernel). With per-launch timing the dependents launch
+    // normally, so each event brackets one kernel. permute_out zeroes the DAG's counters.
+    permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, nullptr, 0);
     ++*launches;
     HMXG_TRY(mark());
     const bool pdl = !time_phases;  // an event between two kernels would break the programmatic edge
-    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
     HMXG_TRY(launch_dependent(pdl, eval_dag, dim3(grid), dim3(kThreads), kSmemBytes, st, tm_wp, tm_t, tm_s, p, dp));
     ++*launches;
     HMXG_TRY(mark());
     HMXG_TRY(launch_dependent(pdl, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp), std::uint64_t(ldq),
-                              static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n, qq));
+                              static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n, qq, d.dag_done,
+                              std::uint64_t(words + 1)));
     ++*launches;
     HMXG_TRY(mark());
     HMXG_CUDA(cudaGetLastError());
+    d.counters_dirty = false;
+    d.last_launches = 3;
     if (time_phases) d.phase_valid = true;
     return HMXG_OK;
   }
+  d.last_fused = false;
   HMXG_TRY(mark());
   const dim3 pgrid((n + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
   if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
@@ -558,8 +620,9 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     ++*launches;
     HMXG_TRY(mark());
   }
-  permute_out<<<pgrid, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq);
+  permute_out<<<pgrid, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq, nullptr, 0);
   ++*launches;
+  d.last_launches = static_cast<std::uint32_t>(lphases.size() + 2);
   HMXG_TRY(mark());
   HMXG_CUDA(cudaGetLastError());
   if (time_phases) d.phase_valid = true;
@@ -891,6 +954,15 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.yp_tiles, plan.yp_tiles.data(), plan.yp_tiles.size(), d.comp));
     HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
+    if (split.nparts == 1) {  // the fused permutations of small problems
+      HMXG_TRY(dev_upload(&d.pmap, plan.pmap.data(), plan.pmap.size(), d.comp));
+      std::vector<uint4> jobs;
+      for (std::uint32_t i = 0; i < plan.num_nodes; ++i)
+        if (cds->lchild[i] == HMXG_NO_NODE && cds->end[i] > cds->start[i])
+          jobs.push_back(make_uint4(i, static_cast<std::uint32_t>(plan.leaf_row[i]), cds->end[i] - cds->start[i], 0u));
+      HMXG_TRY(dev_upload(&d.leaf_jobs, jobs.data(), jobs.size(), d.comp));
+      d.njobs = static_cast<std::uint32_t>(jobs.size());
+    }
     {
       const char* pz = std::getenv("HMXG_POISON");
       d.poison = split.nparts == 1 && pz && *pz && std::strcmp(pz, "0") != 0;
@@ -1217,7 +1289,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
     // Y' rows of other parts' leaves stay zero so the parts' Y sum to the full Y
     HMXG_CUDA(cudaMemsetAsync(d.t, 0, plan.skel_rows * ldq * sizeof(double), st));
     HMXG_CUDA(cudaMemsetAsync(d.yp, 0, plan.rows_pad * ldq * sizeof(double), st));
-    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, dag_done_words(plan, q) * sizeof(std::uint32_t), st));
+    HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, (dag_done_words(plan, q) + 1) * sizeof(std::uint32_t), st));
     permute_in<<<pgrid, 256, 0, st>>>(W, ldw, d.ipmap, d.wp, ldq, nn, qq, nullptr, 0);
   } else if (!plan.remote_t_nodes.empty()) {
     // T of the other parts' nodes arrived through the exchange: mark it complete
@@ -1229,7 +1301,9 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
     eval_dag<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
   }
-  if (stage == 1) permute_out<<<pgrid, 256, 0, st>>>(d.yp, ldq, d.ipmap, Y, ldy, nn, qq);
+  if (stage == 1)  // zeroes the counters for the next evaluation (stage 0 sets them itself)
+    permute_out<<<pgrid, 256, 0, st>>>(d.yp, ldq, d.ipmap, Y, ldy, nn, qq, d.dag_done,
+                                       dag_done_words(plan, q) + 1);
   HMXG_CUDA(cudaGetLastError());
   HMXG_CUDA(cudaStreamSynchronize(st));
   return HMXG_OK;
@@ -1274,7 +1348,8 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   info->v_elems = p.v_elems;
   info->skel_rows = p.skel_rows;
   info->num_devices = static_cast<std::uint32_t>(mat->devs.size());
-  info->launches_per_eval = 3;  // permute-in, eval_dag, permute-out
+  // permute-in, eval_dag, permute-out; 1 when the last evaluation fused the permutations
+  info->launches_per_eval = mat->devs.empty() ? 3 : mat->devs[0].last_launches;
   info->flops_per_col = 2.0 * (2.0 * p.v_elems + p.b_elems + p.d_elems);
   for (const Phase& ph : p.phases) info->exec_flops_per_col += ph.flops_per_col;
   info->device_bytes = mat->devs.empty() ? 0 : mat->devs[0].resident_bytes;
@@ -1286,18 +1361,20 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
 int hmxg_phase_count(const hmxg_mat* mat) {
   if (!mat) return -1;
   const DevState& d = mat->devs[0];
-  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q, d.gemm_grid).size() + 2) : 3;
+  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q, d.gemm_grid).size() + 2)
+                       : (d.last_fused ? 1 : 3);
 }
 
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
   const Plan& p = mat->plan;
   const bool levels = mat->devs[0].last_levels;
+  const bool fused = !levels && mat->devs[0].last_fused;
   const std::vector<const Phase*> lphases = level_phases(p, mat->devs[0].last_q, mat->devs[0].gemm_grid);
-  const std::uint32_t count = static_cast<std::uint32_t>(levels ? lphases.size() + 2 : 3);
+  const std::uint32_t count = static_cast<std::uint32_t>(levels ? lphases.size() + 2 : (fused ? 1 : 3));
   if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
   std::memset(out, 0, sizeof *out);
-  if (!levels && idx == 1) {  // the whole-evaluation DAG launch: every GEMM tile
+  if (fused || (!levels && idx == 1)) {  // the whole-evaluation DAG launch: every GEMM tile
     out->kind = 5;
     for (const Phase* php : lphases) {
       const Phase& ph = *php;
@@ -1305,6 +1382,10 @@ int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
       out->flops_per_col += ph.flops_per_col;
       out->gen_bytes += ph.gen_bytes;
       out->io_bytes_per_col += ph.io_bytes_per_col;
+    }
+    if (fused) {  // the permutations ran inside: W read and Y written once more per column
+      out->io_bytes_per_col += 16.0 * p.n;
+      out->gen_bytes += 4.0 * p.n;
     }
   } else if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
     out->kind = idx == 0 ? 0 : 4;
@@ -1386,9 +1467,14 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
         if (ei != cudaSuccess) return cuda_fail(ei, "cudaGraphInstantiate");
         d.gkey = key;
         d.glaunches = captured;
+        d.gfused = d.last_fused;
       }
       HMXG_CUDA(cudaGraphLaunch(d.gexec, st));
       launches += d.glaunches;
+      d.phase_valid = time_phases;  // the graph's event nodes time this replay
+      d.last_fused = d.gfused;      // and the launch sequence is the captured one
+      d.last_launches = d.glaunches;
+      d.last_q = q;
     }
     if (sync) {
       HMXG_CUDA(cudaEventRecord(d.ev1, st));

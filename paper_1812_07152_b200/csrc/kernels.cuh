@@ -70,6 +70,10 @@ struct GemmParams {
   std::uint64_t ld[kNumBufs];
   std::uint32_t q;
   const std::uint32_t* idmap;   // identity-row sources of the tasks (Task::id_off)
+  // fused permutations (eval_dag's small-problem mode): final leaf rows go to Y[pmap[row], :]
+  double* y_final;              // null: every task stores into its C buffer
+  std::uint64_t ldy;
+  const std::uint32_t* pmap;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -617,6 +621,21 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, true);
   }
 
+  if (p.y_final && (task.flags & kTaskFinal)) {  // scattered into the caller's column-major Y
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = (2 * i + wm) * 8 + fr;
+      if (row >= task.m) continue;
+      double* ycol = p.y_final + __ldg(p.pmap + task.c_row + row) + static_cast<std::uint64_t>(c0) * p.ldy;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = (2 * j + wn) * 8 + 2 * fk;
+        if (col < static_cast<int>(ncols)) ycol[static_cast<std::uint64_t>(col) * p.ldy] = acc[i][j][0];
+        if (col + 1 < static_cast<int>(ncols)) ycol[static_cast<std::uint64_t>(col + 1) * p.ldy] = acc[i][j][1];
+      }
+    }
+    return;
+  }
   double* C = pick_buf(p, task.cbuf);
   const std::uint64_t ldc = pick_ld(p, task.cbuf);
 #pragma unroll
@@ -704,6 +723,24 @@ struct DagParams {
   std::uint32_t ncb, nodes;
   std::uint32_t signal_yp;        // the split leaf variant runs: Yp tiles are waited on
   std::uint32_t fwd_signals;      // the producer lane publishes the stored tiles (wide DAGs)
+  // Small problems (fused): the permutations run inside this launch. The consumer warps
+  // first gather W into Wp for (leaf, column block) jobs, each published on its own counter
+  // (done_w), and the tasks that write final leaf rows (kTaskFinal) store them straight into
+  // Y through pmap. One launch instead of three: the two kernel boundaries and the
+  // permute kernels' fixed latency were a quarter of cfg1's step.
+  std::uint32_t fused;
+  std::uint32_t njobs;            // leaves: jobs are (leaf, column block), leaf-major
+  const uint4* leaf_jobs;         // {leaf node, first Wp row, rows, 0}
+  const double* w;
+  std::uint64_t ldw;
+  double* y;
+  std::uint64_t ldy;
+  const std::uint32_t* pmap;      // Wp / Yp row -> original point
+  // The last CTA to finish zeroes the claim and completion counters for the next launch
+  // (reset_words of them from `claim`, then the exit counter itself); 0: counters are left
+  // as they are (the split fallback's stage 0, whose T counters stage 1 reads).
+  std::uint32_t reset_words;
+  std::uint32_t* exit_ctr;
 #ifdef HMXG_TRACE
   // diagnostic builds (tools/dag_trace.py): per claimed item, kTraceWords globaltimer stamps
   unsigned long long* trace;
@@ -785,6 +822,23 @@ __device__ __forceinline__ void warp_wait(const std::uint32_t* counter, std::uin
   __syncwarp();
 }
 
+// End of an eval_dag CTA: the CTA's warps meet; the last CTA of the grid to get here (every
+// other CTA has stopped reading the counters) zeroes them for the next launch.
+__device__ __forceinline__ void dag_exit(const DagParams& d) {
+  __shared__ std::uint32_t last;
+  __syncthreads();
+  if (d.reset_words == 0) return;
+  if (threadIdx.x == 0) {
+    std::uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(d.exit_ctr) : "memory");
+    last = old + 1 == gridDim.x;
+  }
+  __syncthreads();
+  if (!last) return;
+  for (std::uint32_t i = threadIdx.x; i < d.reset_words; i += blockDim.x) d.claim[i] = 0u;
+  if (threadIdx.x == 0) *d.exit_ctr = 0u;
+}
+
 __global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
 eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
          const __grid_constant__ CUtensorMap tm_s, const GemmParams p, const DagParams d) {
@@ -797,6 +851,43 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   std::uint32_t* const done_t = d.done;
   std::uint32_t* const done_s = done_t + static_cast<std::uint64_t>(d.nodes) * d.ncb;
   std::uint32_t* const done_y = done_s + static_cast<std::uint64_t>(d.nodes) * d.ncb;
+  std::uint32_t* const done_w = done_y + static_cast<std::uint64_t>(d.nodes) * d.ncb;
+
+  if (d.fused && warp < kConsumerWarps) {
+    // Wp[row][phys(c)] = W[pmap[row] + c ldw] for every (leaf, column block) job of this CTA;
+    // 8 loads in flight per thread before the stores (the reads are scattered 8-byte words)
+    const int tid = threadIdx.x;  // 0 .. 127
+    for (std::uint32_t job = blockIdx.x; job < d.njobs * d.ncb; job += gridDim.x) {
+      const uint4 lj = d.leaf_jobs[job / d.ncb];
+      const std::uint32_t cb = job % d.ncb;
+      const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - cb * kBN);
+      const std::uint32_t elems = lj.z * ncols;
+      for (std::uint32_t e0 = 0; e0 < elems; e0 += 8 * kConsumerWarps * 32) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const std::uint32_t e = e0 + u * kConsumerWarps * 32 + tid;
+          if (e < elems) {
+            const std::uint32_t r = e / ncols, c = e % ncols;
+            v[u] = __ldg(d.w + d.pmap[lj.y + r] + static_cast<std::uint64_t>(cb * kBN + c) * d.ldw);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const std::uint32_t e = e0 + u * kConsumerWarps * 32 + tid;
+          if (e < elems) {
+            const std::uint32_t r = e / ncols, c = e % ncols;
+            p.buf[kBufWp][static_cast<std::uint64_t>(lj.y + r) * p.ld[kBufWp] + cb * kCbPitch + c] = v[u];
+          }
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+      if (tid == 0) {
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        red_release_gpu(done_w + static_cast<std::uint64_t>(lj.x) * d.ncb + cb, 1u);
+      }
+    }
+  }
 
   if (warp == kConsumerWarps) {
     if (lane == 0) {
@@ -839,9 +930,13 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         if (end) break;
         const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
         produce_gemm_tile(p, c, rs, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
-          if (sg.bbuf == kBufWp) return;  // Wp is complete: permute_in ran before this launch
-          spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
-                         d.node_tiles[sg.src] * kConsumerWarps, service);
+          if (sg.bbuf == kBufWp) {
+            if (!d.fused) return;  // Wp is complete: permute_in ran before this launch
+            spin_until_svc(done_w + static_cast<std::uint64_t>(sg.src) * d.ncb + cb, 1u, service);
+          } else {
+            spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
+                           d.node_tiles[sg.src] * kConsumerWarps, service);
+          }
           // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
           HMXG_STAMP(seq, 7);
@@ -856,6 +951,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         if (++polls > (1u << 26)) __trap();
       }
     }
+    dag_exit(d);
     return;
   }
   // consumer warps: hand an item's stored tile (or, with kSigEnd, the end) to the producer
@@ -896,7 +992,10 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         wait_for(done_y + static_cast<std::uint64_t>(t.node) * d.ncb + cb, d.yp_tiles[t.node] * kConsumerWarps);
         return;
       }
-      if (t.id_buf == kBufWp) return;
+      if (t.id_buf == kBufWp) {
+        if (d.fused && t.id_node0 != kNoMap) wait_for(done_w + static_cast<std::uint64_t>(t.id_node0) * d.ncb + cb, 1u);
+        return;
+      }
       for (const std::uint32_t node : {t.id_node0, t.id_node1})
         if (node != kNoMap)
           wait_for((t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb,
@@ -925,6 +1024,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       warp_signal(ctr);
     if (stamp) HMXG_STAMP(seq, 5);
   }
+  dag_exit(d);
 }
 
 // Race detector of debug runs (HMXG_POISON=1): every live row of a workspace buffer (the
@@ -988,11 +1088,18 @@ __global__ void __launch_bounds__(256) permute_in(const double* __restrict__ w, 
 }
 
 // Inverse: Y[r, c] = Yp[ipmap[r], c] (point rows read whole, columns of Y written whole).
+// `zero` (optional): eval_dag's counters, zeroed for the next launch once the DAG finished.
 __global__ void __launch_bounds__(256) permute_out(const double* __restrict__ yp, std::uint64_t ldyp,
                                                    const std::uint32_t* __restrict__ ipmap, double* __restrict__ y,
-                                                   std::uint64_t ldy, std::uint32_t n, std::uint32_t q) {
+                                                   std::uint64_t ldy, std::uint32_t n, std::uint32_t q,
+                                                   std::uint32_t* __restrict__ zero, std::uint64_t nzero) {
   __shared__ double tile[kTT][kTT + 1];
   pdl_wait();  // Yp is complete (a no-op without programmatic launch)
+  if (zero) {
+    const std::uint64_t nb = static_cast<std::uint64_t>(gridDim.x) * gridDim.y;
+    const std::uint64_t b = blockIdx.y * static_cast<std::uint64_t>(gridDim.x) + blockIdx.x;
+    for (std::uint64_t i = b * blockDim.x + threadIdx.x; i < nzero; i += nb * blockDim.x) zero[i] = 0u;
+  }
   const std::uint32_t r0 = blockIdx.x * kTT, c0 = blockIdx.y * kTT;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll

@@ -389,7 +389,8 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
             const std::uint32_t pos = leaf_col_src[i][oldrow(i, r)];
             if (pos != kNoMap) cur_id[r] = static_cast<std::uint32_t>(plan.leaf_row[i] + lpt_pos[i][pos]);
           }
-          cur_id_buf = kBufWp;  // complete before the launch: no wait
+          cur_id_buf = kBufWp;  // complete before the launch, or (fused permutes) the leaf's own rows
+          cur_id_node0 = i;
         }
         if (!is_leaf(i) && !colsrc[i].empty()) {  // T_i(j) += T_child(copied row)
           cur_id.assign(v.sranks[i], kNoMap);
@@ -406,7 +407,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         add_tiles(v.sranks[i], kBufT, plan.node_off[i], [&](std::uint32_t r0, std::uint32_t m) {
           // A = V_i^T: tile row r is column oldrow(i, r) of V_i
           if (is_leaf(i)) {  // K: the leaf's dense points (a prefix of its rows)
-            push_seg(kGenV, true, vo, lda, dense_pts[i], m, kBufWp, plan.leaf_row[i], 0, r0, map_off[i], pt_map_off[i],
+            push_seg(kGenV, true, vo, lda, dense_pts[i], m, kBufWp, plan.leaf_row[i], i, r0, map_off[i], pt_map_off[i],
                      m);
           } else {
             const std::uint32_t lc = v.lchild[i], rc = v.rchild[i];
@@ -493,14 +494,14 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     add_tiles(m, kBufYp, plan.leaf_row[i], [&](std::uint32_t r0, std::uint32_t mt) {
       for (std::uint64_t s : near_of[i]) {
         const std::uint32_t j = v.near_pairs[2 * s + 1];
-        push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], 0, r0, pt_map_off[i],
+        push_seg(kGenD, false, v.dptr[s], m, size_of(j), mt, kBufWp, plan.leaf_row[j], j, r0, pt_map_off[i],
                  pt_map_off[j], mt);
       }
       if (active(i))  // the V_i product covers the dense points (a prefix of the rows)
         push_seg(kGenV, false, v.vptr[vslot[i]], m, v.sranks[i], mt, kBufS, plan.node_off[i], i, r0, pt_map_off[i],
                  map_off[i], dense_pts[i] > r0 ? dense_pts[i] - r0 : 0);
     }, plan.phases.back());
-    for (std::uint32_t t = t0; t < plan.tasks.size(); ++t) plan.tasks[t].flags |= kTaskIdLast;
+    for (std::uint32_t t = t0; t < plan.tasks.size(); ++t) plan.tasks[t].flags |= kTaskIdLast | kTaskFinal;
     leaf_tasks_of.push_back({i, t0, static_cast<std::uint32_t>(plan.tasks.size())});
   }
   close_phase();
@@ -520,7 +521,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       // skeleton-row copies: both belong to the leaf task below
       if (has_v_seg(nt)) nt.seg_end -= 1;
       nt.id_off = nt.id_node0 = nt.id_node1 = kNoMap;
-      nt.flags = 0;
+      nt.flags = with_v ? 0 : kTaskFinal;  // an inactive leaf's near rows are its final rows
       plan.tasks.push_back(nt);
     }
   }

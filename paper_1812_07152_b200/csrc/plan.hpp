@@ -108,6 +108,10 @@ constexpr std::uint16_t kTaskIdLast = 2;
 // producer acquired that node's completion before streaming it, and the stage barriers
 // (arrive: release, wait: acquire) carry it to the consumers, which skip their own poll.
 constexpr std::uint16_t kTaskIdSynced = 4;
+// The task writes the final value of its Yp rows (the combined leaf tasks, the split
+// variant's accumulating leaf tasks, and the near tasks of leaves without a basis): with the
+// fused permutations (eval_dag's small-problem mode) they are stored straight into Y.
+constexpr std::uint16_t kTaskFinal = 8;
 
 // kPhaseNear: Y'_i = sum_j D_ij Wp_j (depends on Wp only); kPhaseLeaf: Y'_i += V_i S_i
 // (accumulates onto the near rows of the same leaf through the task's identity rows).
