@@ -240,7 +240,9 @@ def _load(path: str, symbols: dict) -> C.CDLL:
         except OSError as e:  # pragma: no cover - depends on the box
             raise NativeLibraryError(f"cannot load {path}: {e}") from e
         for name, (res, args) in symbols.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)  # an older A/B build (HMXG_LIBRARY) may lack newer entry points
+            if fn is None:
+                continue
             fn.restype = res
             fn.argtypes = args
         _libs[path] = lib

@@ -100,8 +100,8 @@ struct DevState {
   std::uint32_t* yp_tiles = nullptr;
   // fused permutations (small problems, see fused_io): padded row -> point, and the leaf jobs
   std::uint32_t* pmap = nullptr;
-  uint4* leaf_jobs = nullptr;
-  std::uint32_t njobs = 0;
+  std::uint32_t* rowleaf = nullptr;    // Wp row -> leaf node
+  std::uint32_t* wp_target = nullptr;  // leaf node -> rows
   // an enqueue failed between eval_dag and the launch that zeroes its counters: zero them first
   bool counters_dirty = false;
   bool last_fused = false;  // the last evaluation ran the single fused launch
@@ -194,8 +194,10 @@ struct DevState {
     ts_live = nullptr;
     cudaFree(pmap);
     pmap = nullptr;
-    cudaFree(leaf_jobs);
-    leaf_jobs = nullptr;
+    cudaFree(rowleaf);
+    rowleaf = nullptr;
+    cudaFree(wp_target);
+    wp_target = nullptr;
     dag_done = nullptr;
     dag_done_cap = 0;
     node_tiles = nullptr;
@@ -296,12 +298,29 @@ std::vector<const Phase*> level_phases(const Plan& plan, std::size_t q, unsigned
     for (const Phase& ph : plan.split_phases) out.push_back(&ph);
   return out;
 }
+// Column-split parts per tile for narrow DAGs (DagParams::colsplit): with fewer work items
+// than resident CTAs the dependency chain of small GEMMs is DMMA-time bound on one SM per
+// tile, so each tile's 64 columns become 4 (or 2) items on different SMs. Wide DAGs keep
+// whole tiles: the split re-reads every A chunk per part. HMXG_COLSPLIT overrides (1, 2, 4).
+std::uint32_t colsplit(const Plan& plan, std::size_t q, unsigned grid, std::uint32_t stage = 0) {
+  if (stage != 0 || plan.nparts != 1) return 1;
+  if (const char* e = std::getenv("HMXG_COLSPLIT")) {
+    const int v = std::atoi(e);
+    return v == 2 || v == 4 ? static_cast<std::uint32_t>(v) : 1u;
+  }
+  std::uint64_t tasks = 0;
+  for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
+  const std::uint64_t items = tasks * ((q + kBN - 1) / kBN);
+  return items < grid ? 4u : (items < 4ull * grid ? 2u : 1u);
+}
 std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage, unsigned grid) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
+  const std::uint32_t S = colsplit(plan, q, grid, stage);
   std::vector<std::uint64_t> items;
   auto emit = [&](std::uint32_t t0, std::uint32_t t1) {
     for (std::uint32_t t = t0; t < t1; ++t)
-      for (std::uint32_t cb = 0; cb < ncb; ++cb) items.push_back(make_item(kItemGemm, cb, t));
+      for (std::uint32_t cb = 0; cb < ncb; ++cb)
+        for (std::uint32_t sub = 0; sub < S; ++sub) items.push_back(make_item(kItemGemm, cb, t, sub));
   };
   const bool split = split_leaf(plan, q, grid);
   std::vector<const Phase*> tree, leaf;
@@ -349,9 +368,19 @@ std::uint32_t forward_signals(std::uint32_t nitems, unsigned grid) {
 // [claim counter per stage | T counters | S counters | Yp counters | Wp counters] (nodes x ncb
 // each), then the exit counter of the launch's self-reset (DagParams::reset_words)
 constexpr std::size_t kDagClaimWords = 2;
-std::size_t dag_done_words(const Plan& plan, std::size_t q) {
+// Words between two counters: polled counters packed into a few L2 lines make those lines'
+// slice a hot spot when hundreds of producers and consumers poll and release them at once
+// (narrow DAGs). HMXG_CSTRIDE overrides.
+std::uint32_t counter_stride(const Plan& plan, std::size_t q, unsigned grid, std::uint32_t stage = 0) {
+  if (stage != 0 || plan.nparts != 1) return 1;
+  if (const char* e = std::getenv("HMXG_CSTRIDE")) return static_cast<std::uint32_t>(std::max(1, std::min(64, std::atoi(e))));
+  // narrow DAGs (the column-split ones): one counter per 128-byte line (cfg1 DAG 63 -> 58 us
+  // with the split); wide DAGs poll few counters at a time and keep them packed
+  return colsplit(plan, q, grid) > 1 ? 32u : 1u;
+}
+std::size_t dag_done_words(const Plan& plan, std::size_t q, std::uint32_t cstride = 1) {
   const std::size_t ncb = (q + kBN - 1) / kBN;
-  return kDagClaimWords + 4 * std::size_t(plan.num_nodes) * ncb;  // T, S, Yp, Wp counters
+  return (kDagClaimWords + 4 * std::size_t(plan.num_nodes) * ncb) * cstride;  // T, S, Yp, Wp counters
 }
 
 // Small problems run the permutations inside the DAG launch (DagParams::fused): one launch,
@@ -384,7 +413,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage, d.gemm_grid);
   if (items.size() >= 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many work items");
   HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
-  const std::size_t words = dag_done_words(plan, q);
+  const std::size_t words = dag_done_words(plan, q, counter_stride(plan, q, d.gemm_grid, stage));
   if (words > d.dag_done_cap) {
     d.drop_graph();
     cudaFree(d.dag_done);
@@ -439,7 +468,7 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
       const std::uint32_t qi = static_cast<std::uint32_t>(r[0]);
       if (qi >= items.size()) continue;
       const std::uint32_t task = static_cast<std::uint32_t>(items[qi]);
-      const std::uint32_t cb = static_cast<std::uint32_t>(items[qi] >> 32) & 0xffffffu;
+      const std::uint32_t cb = item_cb(items[qi]);
       int kind = -1, level = -1;
       for (const Phase* ph : phs)
         if (task >= ph->task_begin && task < ph->task_end) {
@@ -454,6 +483,16 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
                    r[7]);
     }
   std::fclose(f);
+  // the fused permute jobs: per CTA start, stores done, signal released
+  const std::string ppath = std::string(path) + ".perm";
+  FILE* fp = std::fopen(ppath.c_str(), "w");
+  if (!fp) return;
+  std::fprintf(fp, "cta,t_start,t_stored,t_signalled\n");
+  for (std::size_t b = 0; b < g_trace_words / (kTraceSeq * kTraceWords); ++b) {
+    const unsigned long long* r = &h[(b * kTraceSeq + kTraceSeq - 1) * kTraceWords];
+    if (r[0] == 0xfffffffffull) std::fprintf(fp, "%zu,%llu,%llu,%llu\n", b, r[1], r[2], r[3]);
+  }
+  std::fclose(fp);
 }
 #endif
 
@@ -529,17 +568,20 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     for (const auto& e : d.dag)
       if (e.items && e.q == q && e.stage == 0) di = &e;
     if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
-    const std::size_t words = dag_done_words(plan, q);
+    const std::uint32_t cst = counter_stride(plan, q, d.gemm_grid);
+    const std::size_t words = dag_done_words(plan, q, cst);
     const bool fused = fused_io(plan, q);
     d.last_fused = fused;
     DagParams dp{};
     dp.items = di->items;
     dp.nitems = di->nitems;
     dp.claim = d.dag_done;
-    dp.done = d.dag_done + kDagClaimWords;
+    dp.done = d.dag_done + kDagClaimWords * cst;
+    dp.cstride = cst;
     dp.node_tiles = d.node_tiles;
     dp.yp_tiles = d.yp_tiles;
     dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
+    dp.colsplit = colsplit(plan, q, d.gemm_grid);
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
     dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);
@@ -554,8 +596,10 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     if (fused) {
       // one launch: permutations inside, counters zeroed by the DAG's last CTA
       dp.fused = 1;
-      dp.njobs = d.njobs;
-      dp.leaf_jobs = d.leaf_jobs;
+      dp.n = n;
+      dp.ipmap = d.ipmap;
+      dp.rowleaf = d.rowleaf;
+      dp.wp_target = d.wp_target;
       dp.w = w;
       dp.ldw = ldw;
       dp.pmap = d.pmap;
@@ -564,7 +608,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       p.y_final = y;
       p.ldy = ldy;
       p.pmap = d.pmap;
-      const unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, d.njobs * dp.ncb));
+      const unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, (n + 31) / 32 * dp.ncb));
       HMXG_TRY(mark());
       eval_dag<<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
       ++*launches;
@@ -956,12 +1000,14 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&d.remote_t, plan.remote_t_nodes.data(), plan.remote_t_nodes.size(), d.comp));
     if (split.nparts == 1) {  // the fused permutations of small problems
       HMXG_TRY(dev_upload(&d.pmap, plan.pmap.data(), plan.pmap.size(), d.comp));
-      std::vector<uint4> jobs;
+      std::vector<std::uint32_t> rowleaf(plan.rows_pad, 0), target(plan.num_nodes, 0);
       for (std::uint32_t i = 0; i < plan.num_nodes; ++i)
-        if (cds->lchild[i] == HMXG_NO_NODE && cds->end[i] > cds->start[i])
-          jobs.push_back(make_uint4(i, static_cast<std::uint32_t>(plan.leaf_row[i]), cds->end[i] - cds->start[i], 0u));
-      HMXG_TRY(dev_upload(&d.leaf_jobs, jobs.data(), jobs.size(), d.comp));
-      d.njobs = static_cast<std::uint32_t>(jobs.size());
+        if (cds->lchild[i] == HMXG_NO_NODE) {
+          target[i] = cds->end[i] - cds->start[i];
+          for (std::uint32_t r = 0; r < target[i]; ++r) rowleaf[plan.leaf_row[i] + r] = i;
+        }
+      HMXG_TRY(dev_upload(&d.rowleaf, rowleaf.data(), rowleaf.size(), d.comp));
+      HMXG_TRY(dev_upload(&d.wp_target, target.data(), target.size(), d.comp));
     }
     {
       const char* pz = std::getenv("HMXG_POISON");
@@ -1133,6 +1179,7 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
   if (nitems) *nitems = items.size();
   const bool split = split_leaf(plan, q, grid);
+  const std::uint32_t S = colsplit(plan, q, grid);  // parts per tile: every tile appears S times
   // (1) every task of the variant that runs, once per column block
   std::vector<std::uint32_t> want(plan.tasks.size(), 0), seen(plan.tasks.size() * std::size_t(ncb), 0);
   for (const Phase& ph : plan.phases)
@@ -1145,14 +1192,17 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   for (const Phase& ph : plan.split_phases)
     if (ph.kind == kPhaseNear)
       for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) is_near[t] = split ? 1 : 0;
+  std::vector<std::uint8_t> seen_sub(plan.tasks.size() * std::size_t(ncb) * S, 0);
   for (std::uint64_t it : items) {
-    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = static_cast<std::uint32_t>(it >> 32) & 0xffffffu;
-    if (t >= plan.tasks.size() || cb >= ncb || !want[t] || seen[std::size_t(t) * ncb + cb]++)
-      return set_err(HMXG_EINVAL, "dag: item list is not the variant's tasks x column blocks");
+    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = item_cb(it), sub = item_sub(it);
+    if (t >= plan.tasks.size() || cb >= ncb || sub >= S || !want[t] ||
+        seen_sub[(std::size_t(t) * ncb + cb) * S + sub]++)
+      return set_err(HMXG_EINVAL, "dag: item list is not the variant's tasks x column blocks x parts");
+    ++seen[std::size_t(t) * ncb + cb];
   }
   for (std::size_t t = 0; t < plan.tasks.size(); ++t)
     for (std::uint32_t cb = 0; cb < ncb; ++cb)
-      if (want[t] && !seen[t * ncb + cb]) return set_err(HMXG_EINVAL, "dag: a task tile is missing");
+      if (want[t] && seen[t * ncb + cb] != S) return set_err(HMXG_EINVAL, "dag: a task tile is missing");
   // (3) the kernel's completion targets are the writer counts
   const std::size_t nn = plan.num_nodes;
   std::vector<std::uint32_t> wr(3 * nn, 0);
@@ -1170,9 +1220,9 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   }
   // (2) topological: every tile an item waits for is complete before it in the claim order
   std::vector<std::uint32_t> done(3 * nn * std::size_t(ncb), 0);
-  auto ready = [&](std::size_t r, std::uint32_t cb) { return done[r * ncb + cb] >= wr[r]; };
+  auto ready = [&](std::size_t r, std::uint32_t cb) { return done[r * ncb + cb] >= wr[r] * S; };
   for (std::uint64_t it : items) {
-    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = static_cast<std::uint32_t>(it >> 32) & 0xffffffu;
+    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = item_cb(it);
     const Task& tk = plan.tasks[t];
     for (std::uint32_t sgi = tk.seg_begin; sgi < tk.seg_end; ++sgi) {
       const SegDev& sg = plan.segs[sgi];
@@ -1272,9 +1322,11 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   dp.nitems = di->nitems;
   dp.claim = d.dag_done + stage;
   dp.done = d.dag_done + kDagClaimWords;
+  dp.cstride = 1;
   dp.node_tiles = d.node_tiles;
   dp.yp_tiles = d.yp_tiles;
   dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
+  dp.colsplit = 1;
   dp.ncb = ncb;
   dp.nodes = plan.num_nodes;
   dp.fwd_signals = forward_signals(di->nitems, d.gemm_grid);

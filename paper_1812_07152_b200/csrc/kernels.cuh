@@ -371,7 +371,7 @@ struct RingSlot {
 };
 static_assert(sizeof(RingSlot) == 192, "RingSlot layout");
 constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * sizeof(RingSlot) +
-                           3 * kSigRing * 8 + 1024;
+                           3 * kSigRing * 8 + 8 + 1024;
 
 struct CtaSmem {
   unsigned char* stage;    // kStages * kStageBytes, 1024-byte aligned
@@ -383,6 +383,7 @@ struct CtaSmem {
   std::uint64_t* sfull;    // [kSigRing] one arrive per consumer warp
   std::uint64_t* sempty;   // [kSigRing] the producer took the record
   std::uint64_t* saddr;    // [kSigRing]
+  std::uint64_t* pbar;     // eval_dag fused mode: the CTA's permute jobs are done (stages free)
 };
 
 __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
@@ -397,6 +398,7 @@ __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
   c.sfull = reinterpret_cast<std::uint64_t*>(c.ring + kTileRing);
   c.sempty = c.sfull + kSigRing;
   c.saddr = c.sempty + kSigRing;
+  c.pbar = c.saddr + kSigRing;
   return c;
 }
 
@@ -414,6 +416,7 @@ __device__ __forceinline__ void init_barriers(const CtaSmem& c) {
       mbar_init(&c.sfull[s], kConsumerWarps);
       mbar_init(&c.sempty[s], 1);
     }
+    mbar_init(c.pbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -517,16 +520,25 @@ struct NoHook {
   template <class... A>
   __device__ void operator()(A...) const {}
 };
+// Column-split items (narrow DAGs, DagParams::colsplit = S): the 64 columns of a tile are S
+// items of 64/S columns on different CTAs, so a short dependency chain of small GEMMs runs
+// on S times as many SMs (the K loop of one tile is the DMMA time of one SM). Item `sub`
+// covers columns [sub 64/S, (sub+1) 64/S) of the block: its warps' fragments shift by that
+// many columns, and only 64/(16 S) fragment columns per warp are live.
 template <class WaitId, class KEnd = NoHook, class KStart = NoHook>
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const RingSlot* rs,
-                                                  const Task& task, std::uint32_t cb, const FragAddr& fa,
+                                                  const Task& task, std::uint32_t cb, const FragAddr& fa0,
                                                   std::uint32_t& it, WaitId&& wait_id, KEnd&& k_end = KEnd{},
-                                                  KStart&& k_start = KStart{}) {
+                                                  KStart&& k_start = KStart{}, std::uint32_t sub = 0,
+                                                  std::uint32_t split = 1) {
+  const std::uint32_t width = kBN / split, cs = sub * width;  // this item's columns in the block
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp & 1, wn = warp >> 1, fr = lane >> 2, fk = lane & 3;
+  FragAddr fa = fa0;
+  fa.b += cs * 8u;
   // Warp-uniform trim of fragments outside the valid rows / the last column block.
-  const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - c0);
+  const std::uint32_t ncols = c0 + cs < p.q ? min(width, p.q - c0 - cs) : 0u;
   const int frag_cols = (static_cast<int>(ncols) + 7) / 8;
   const int live_j = min(4, max(0, (frag_cols - wn + 1) / 2));
 
@@ -546,7 +558,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (src[i] == kNoMap) continue;
-      const double* srow = B + static_cast<std::uint64_t>(src[i]) * ldb + cb * kCbPitch;
+      const double* srow = B + static_cast<std::uint64_t>(src[i]) * ldb + cb * kCbPitch + cs;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int col = (2 * j + wn) * 8 + 2 * fk;
@@ -603,13 +615,28 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     const int live_i = min(4, max(0, ((rows + 7) / 8 - wm + 1) / 2));
     const std::uint32_t nch = sg.nchunks;
     const int lks = sg.last_ksteps;
-    if (live_j == 4) {
+    if (live_i <= 0 || live_j <= 0) {
+      consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it);
+    } else if (live_j == 4) {
       switch (live_i) {
         case 4: consume_chunks<4, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         case 3: consume_chunks<3, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
-        case 1: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
-        default: consume_chunks<0, 0>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        default: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+      }
+    } else if (live_j == 1 && split == 4) {  // column-split items: one live fragment column
+      switch (live_i) {
+        case 4: consume_chunks<4, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 3: consume_chunks<3, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 2: consume_chunks<2, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        default: consume_chunks<1, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+      }
+    } else if (live_j == 2 && split == 2) {
+      switch (live_i) {
+        case 4: consume_chunks<4, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 3: consume_chunks<3, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        case 2: consume_chunks<2, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
+        default: consume_chunks<1, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
       }
     } else {
       consume_chunks_pred(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it, live_i, live_j);
@@ -626,7 +653,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     for (int i = 0; i < 4; ++i) {
       const int row = (2 * i + wm) * 8 + fr;
       if (row >= task.m) continue;
-      double* ycol = p.y_final + __ldg(p.pmap + task.c_row + row) + static_cast<std::uint64_t>(c0) * p.ldy;
+      double* ycol = p.y_final + __ldg(p.pmap + task.c_row + row) + static_cast<std::uint64_t>(c0 + cs) * p.ldy;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int col = (2 * j + wn) * 8 + 2 * fk;
@@ -642,7 +669,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
   for (int i = 0; i < 4; ++i) {
     const int row = (2 * i + wm) * 8 + fr;
     if (row >= task.m) continue;
-    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + cb * kCbPitch;  // point major
+    double* crow = C + static_cast<std::uint64_t>(task.c_row + row) * ldc + cb * kCbPitch + cs;  // point major
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = (2 * j + wn) * 8 + 2 * fk;
@@ -709,8 +736,17 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
 // (T or S). There are no level boundaries: a level's first tiles start while the
 // previous level's last tiles finish, and there is one launch instead of ~2H.
 enum ItemKind : std::uint32_t { kItemGemm = 0, kItemEnd = 3 };
-__host__ __device__ __forceinline__ std::uint64_t make_item(std::uint32_t kind, std::uint32_t cb, std::uint32_t idx) {
-  return (static_cast<std::uint64_t>(kind) << 56) | (static_cast<std::uint64_t>(cb) << 32) | idx;
+// item word: kind (bits 56-63), column-split part (48-55), column block (32-47), task (0-31)
+__host__ __device__ __forceinline__ std::uint64_t make_item(std::uint32_t kind, std::uint32_t cb, std::uint32_t idx,
+                                                            std::uint32_t sub = 0) {
+  return (static_cast<std::uint64_t>(kind) << 56) | (static_cast<std::uint64_t>(sub) << 48) |
+         (static_cast<std::uint64_t>(cb) << 32) | idx;
+}
+__host__ __device__ __forceinline__ std::uint32_t item_cb(std::uint64_t item) {
+  return static_cast<std::uint32_t>(item >> 32) & 0xffffu;
+}
+__host__ __device__ __forceinline__ std::uint32_t item_sub(std::uint64_t item) {
+  return static_cast<std::uint32_t>(item >> 48) & 0xffu;
 }
 
 struct DagParams {
@@ -722,6 +758,8 @@ struct DagParams {
   const std::uint32_t* yp_tiles;  // near-phase row tiles per leaf
   std::uint32_t ncb, nodes;
   std::uint32_t signal_yp;        // the split leaf variant runs: Yp tiles are waited on
+  std::uint32_t colsplit;         // column-split parts per tile (1, 2 or 4): targets x colsplit
+  std::uint32_t cstride;          // words between counters (narrow DAGs: one per 128-byte line)
   std::uint32_t fwd_signals;      // the producer lane publishes the stored tiles (wide DAGs)
   // Small problems (fused): the permutations run inside this launch. The consumer warps
   // first gather W into Wp for (leaf, column block) jobs, each published on its own counter
@@ -729,8 +767,10 @@ struct DagParams {
   // Y through pmap. One launch instead of three: the two kernel boundaries and the
   // permute kernels' fixed latency were a quarter of cfg1's step.
   std::uint32_t fused;
-  std::uint32_t njobs;            // leaves: jobs are (leaf, column block), leaf-major
-  const uint4* leaf_jobs;         // {leaf node, first Wp row, rows, 0}
+  std::uint32_t n;                // points (rows of W)
+  const std::uint32_t* ipmap;     // point -> Wp row
+  const std::uint32_t* rowleaf;   // Wp row -> leaf node
+  const std::uint32_t* wp_target; // per leaf: its rows (the done_w count of a complete block)
   const double* w;
   std::uint64_t ldw;
   double* y;
@@ -848,45 +888,68 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   pdl_trigger();  // permute_out may launch; it waits for this grid before reading Yp
   pdl_wait();     // Wp and the zeroed counters of permute_in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint64_t cst = d.cstride, region = static_cast<std::uint64_t>(d.nodes) * d.ncb * cst;
   std::uint32_t* const done_t = d.done;
-  std::uint32_t* const done_s = done_t + static_cast<std::uint64_t>(d.nodes) * d.ncb;
-  std::uint32_t* const done_y = done_s + static_cast<std::uint64_t>(d.nodes) * d.ncb;
-  std::uint32_t* const done_w = done_y + static_cast<std::uint64_t>(d.nodes) * d.ncb;
+  std::uint32_t* const done_s = done_t + region;
+  std::uint32_t* const done_y = done_s + region;
+  std::uint32_t* const done_w = done_y + region;
+  auto at = [&](std::uint32_t node, std::uint32_t cb) { return (static_cast<std::uint64_t>(node) * d.ncb + cb) * cst; };
+  const std::uint32_t wmul = kConsumerWarps * d.colsplit;  // signals per complete row tile
 
   if (d.fused && warp < kConsumerWarps) {
-    // Wp[row][phys(c)] = W[pmap[row] + c ldw] for every (leaf, column block) job of this CTA;
-    // 8 loads in flight per thread before the stores (the reads are scattered 8-byte words)
+    // Wp[ipmap[r]][phys(c)] = W[r + c ldw] in source order: a job is 32 consecutive points x
+    // one column block, read as whole 256-byte column segments, transposed through shared
+    // memory (the stage buffers: this CTA's producer issues no chunk before pbar) and written
+    // as whole point rows; each of the job's points then counts toward its leaf's done_w.
+    // One HBM round trip per job instead of the dependent pmap -> W gathers.
     const int tid = threadIdx.x;  // 0 .. 127
-    for (std::uint32_t job = blockIdx.x; job < d.njobs * d.ncb; job += gridDim.x) {
-      const uint4 lj = d.leaf_jobs[job / d.ncb];
-      const std::uint32_t cb = job % d.ncb;
+    double* tile = reinterpret_cast<double*>(c.stage);  // 32 x 65
+    std::uint32_t* rows = reinterpret_cast<std::uint32_t*>(tile + 32 * 65);  // Wp rows of the job
+#ifdef HMXG_TRACE
+    unsigned long long* ptr_ = d.trace + (static_cast<std::uint64_t>(blockIdx.x) * kTraceSeq + kTraceSeq - 1) * kTraceWords;
+    if (tid == 0) ptr_[1] = gtimer();
+#endif
+    const std::uint32_t nblk = (d.n + 31) / 32;
+    for (std::uint32_t job = blockIdx.x; job < nblk * d.ncb; job += gridDim.x) {
+      const std::uint32_t r0 = (job / d.ncb) * 32, cb = job % d.ncb;
       const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - cb * kBN);
-      const std::uint32_t elems = lj.z * ncols;
-      for (std::uint32_t e0 = 0; e0 < elems; e0 += 8 * kConsumerWarps * 32) {
-        double v[8];
+      const std::uint32_t nr = min(32u, d.n - r0);
+      double v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const std::uint32_t e = e0 + u * kConsumerWarps * 32 + tid;
-          if (e < elems) {
-            const std::uint32_t r = e / ncols, c = e % ncols;
-            v[u] = __ldg(d.w + d.pmap[lj.y + r] + static_cast<std::uint64_t>(cb * kBN + c) * d.ldw);
-          }
-        }
+      for (int u = 0; u < 16; ++u) {
+        const std::uint32_t e = u * 128 + tid, r = e & 31, cc = e >> 5;
+        v[u] = (r < nr && cc < ncols) ? __ldg(d.w + r0 + r + static_cast<std::uint64_t>(cb * kBN + cc) * d.ldw) : 0.0;
+      }
+      if (tid < 32) rows[tid] = tid < static_cast<int>(nr) ? __ldg(d.ipmap + r0 + tid) : 0u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const std::uint32_t e = e0 + u * kConsumerWarps * 32 + tid;
-          if (e < elems) {
-            const std::uint32_t r = e / ncols, c = e % ncols;
-            p.buf[kBufWp][static_cast<std::uint64_t>(lj.y + r) * p.ld[kBufWp] + cb * kCbPitch + c] = v[u];
-          }
-        }
+      for (int u = 0; u < 16; ++u) {
+        const std::uint32_t e = u * 128 + tid;
+        tile[(e & 31) * 65 + (e >> 5)] = v[u];
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
-      if (tid == 0) {
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-        red_release_gpu(done_w + static_cast<std::uint64_t>(lj.x) * d.ncb + cb, 1u);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const std::uint32_t e = u * 128 + tid, cc = e & 63, r = e >> 6;
+        if (r < nr && cc < ncols)
+          p.buf[kBufWp][static_cast<std::uint64_t>(rows[r]) * p.ld[kBufWp] + cb * kCbPitch + cc] = tile[r * 65 + cc];
       }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+#ifdef HMXG_TRACE
+      if (tid == 0) ptr_[2] = gtimer();
+#endif
+      if (tid < static_cast<int>(nr)) {  // the CTA's stores (bar.sync above) before this point's release
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        red_release_gpu(done_w + at(__ldg(d.rowleaf + rows[tid]), cb), 1u);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");  // tile / rows reuse
     }
+#ifdef HMXG_TRACE
+    if (tid == 0) {
+      ptr_[3] = gtimer();
+      ptr_[0] = 0xfffffffffull;  // marks the permute record (not an item)
+    }
+#endif
+    if (tid == 0) mbar_arrive(c.pbar);  // the stage buffers are the producer's again
   }
 
   if (warp == kConsumerWarps) {
@@ -915,6 +978,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         }
       };
       std::uint32_t it = 0;
+      bool stages_free = !d.fused;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t q = atomicAdd(d.claim, 1u);
         const std::uint64_t item = q < d.nitems ? d.items[q] : make_item(kItemEnd, 0, 0);
@@ -928,14 +992,18 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         const bool end = static_cast<std::uint32_t>(item >> 56) == kItemEnd;
         const RingSlot* rs = post_item(p, c, seq, item, end, static_cast<std::uint32_t>(item), service);
         if (end) break;
-        const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
+        const std::uint32_t cb = item_cb(item);
+        if (!stages_free) {  // fused mode: the consumers' permute jobs use the stage buffers
+          mbar_wait_svc(c.pbar, 0, service);
+          stages_free = true;
+        }
         produce_gemm_tile(p, c, rs, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
           if (sg.bbuf == kBufWp) {
             if (!d.fused) return;  // Wp is complete: permute_in ran before this launch
-            spin_until_svc(done_w + static_cast<std::uint64_t>(sg.src) * d.ncb + cb, 1u, service);
+            spin_until_svc(done_w + at(sg.src, cb), d.wp_target[sg.src], service);
           } else {
-            spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(sg.src) * d.ncb + cb,
-                           d.node_tiles[sg.src] * kConsumerWarps, service);
+            spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + at(sg.src, cb),
+                           d.node_tiles[sg.src] * wmul, service);
           }
           // generic-proxy stores of other CTAs, acquired above, before our async-proxy reads
           asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -977,7 +1045,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     }
     const bool stamp = threadIdx.x == 0;
     if (stamp) HMXG_STAMP(seq, 3);
-    const std::uint32_t cb = static_cast<std::uint32_t>(item >> 32) & 0xffffffu;
+    const std::uint32_t cb = item_cb(item), sub = item_sub(item);
     const Task task = rs->task;
     consume_gemm_tile(p, c, rs, task, cb, fa, it, [&](const Task& t, bool own_rows) {
       // the rows about to be read are complete for this column block (every lane acquires;
@@ -989,17 +1057,18 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         (void)ld_acquire(ctr);
       };
       if (own_rows) {
-        wait_for(done_y + static_cast<std::uint64_t>(t.node) * d.ncb + cb, d.yp_tiles[t.node] * kConsumerWarps);
+        wait_for(done_y + at(t.node, cb), d.yp_tiles[t.node] * wmul);
         return;
       }
       if (t.id_buf == kBufWp) {
-        if (d.fused && t.id_node0 != kNoMap) wait_for(done_w + static_cast<std::uint64_t>(t.id_node0) * d.ncb + cb, 1u);
+        if (d.fused && t.id_node0 != kNoMap)
+          wait_for(done_w + at(t.id_node0, cb), d.wp_target[t.id_node0]);
         return;
       }
       for (const std::uint32_t node : {t.id_node0, t.id_node1})
         if (node != kNoMap)
-          wait_for((t.id_buf == kBufT ? done_t : done_s) + static_cast<std::uint64_t>(node) * d.ncb + cb,
-                   d.node_tiles[node] * kConsumerWarps);
+          wait_for((t.id_buf == kBufT ? done_t : done_s) + at(node, cb),
+                   d.node_tiles[node] * wmul);
     }, [&]() {
       if (stamp) HMXG_STAMP(seq, 4);
     }, [&](std::uint32_t it0) {
@@ -1011,13 +1080,13 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
 #else
       (void)it0;
 #endif
-    });
+    }, sub, d.colsplit);
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
     release_item(c, seq);
-    const bool publish = task.cbuf != kBufYp || d.signal_yp;
-    std::uint32_t* const ctr = (task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) +
-                               static_cast<std::uint64_t>(task.node) * d.ncb + cb;
+    // final leaf rows have no reader inside the launch (the split variant's near rows do)
+    const bool publish = task.cbuf != kBufYp || (d.signal_yp && !(task.flags & kTaskFinal));
+    std::uint32_t* const ctr = (task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) + at(task.node, cb);
     if (d.fwd_signals)
       post_signal(seq, publish ? reinterpret_cast<std::uint64_t>(ctr) : 0);
     else if (publish)

@@ -64,6 +64,14 @@ def summarize(path: str) -> None:
         dp = sum(dp) / len(dp) / 1e3 if dp else float("nan")
         print(f"{KIND.get(k[0], k[0]):>6} L{k[1]:<2} {n:>6} {ch:6.1f} {first:8.2f} {last:8.2f} {ct:10.2f} {tk:10.2f} "
               f"{kd:10.2f} {t1:9.2f} {dp:10.2f}")
+    if os.path.exists(path + ".perm"):  # fused permute jobs (small problems)
+        pr = list(csv.DictReader(open(path + ".perm")))
+        if pr:
+            st = [(int(r["t_start"]) - t0) / 1e3 for r in pr]
+            sd = [(int(r["t_stored"]) - t0) / 1e3 for r in pr]
+            sg = [(int(r["t_signalled"]) - t0) / 1e3 for r in pr]
+            print(f"  permute jobs: {len(pr)} CTAs, start {min(st):.2f}..{max(st):.2f}, stored {min(sd):.2f}..{max(sd):.2f}, "
+                  f"signalled {min(sg):.2f}..{max(sg):.2f} us")
 
 
 if __name__ == "__main__":
