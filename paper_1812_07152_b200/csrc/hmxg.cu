@@ -610,7 +610,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       p.pmap = d.pmap;
       const unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, (n + 31) / 32 * dp.ncb));
       HMXG_TRY(mark());
-      eval_dag<<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+      eval_dag<true><<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
       ++*launches;
       HMXG_TRY(mark());
       HMXG_CUDA(cudaGetLastError());
@@ -629,7 +629,9 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     ++*launches;
     HMXG_TRY(mark());
     const bool pdl = !time_phases;  // an event between two kernels would break the programmatic edge
-    HMXG_TRY(launch_dependent(pdl, eval_dag, dim3(grid), dim3(kThreads), kSmemBytes, st, tm_wp, tm_t, tm_s, p, dp));
+    const bool narrow = dp.colsplit > 1 || dp.cstride > 1;
+    HMXG_TRY(launch_dependent(pdl, narrow ? eval_dag<true> : eval_dag<false>, dim3(grid), dim3(kThreads), kSmemBytes,
+                              st, tm_wp, tm_t, tm_s, p, dp));
     ++*launches;
     HMXG_TRY(mark());
     HMXG_TRY(launch_dependent(pdl, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp), std::uint64_t(ldq),
@@ -947,12 +949,16 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3);
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    HMXG_CUDA(cudaFuncSetAttribute(eval_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_CUDA(cudaFuncSetAttribute(eval_dag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    HMXG_CUDA(cudaFuncSetAttribute(eval_dag<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     {
       int per_sm = 0, sms = 0;
       int per_sm_dag = 0;
       HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grouped_gemm, kThreads, kSmemBytes));
-      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dag, eval_dag, kThreads, kSmemBytes));
+      int per_sm_narrow = 0;
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_dag, eval_dag<false>, kThreads, kSmemBytes));
+      HMXG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_narrow, eval_dag<true>, kThreads, kSmemBytes));
+      per_sm_dag = std::min(per_sm_dag, per_sm_narrow);
       // eval_dag relies on every CTA of its grid being resident (items wait on earlier items)
       per_sm = std::min(per_sm, per_sm_dag);
       HMXG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.dev));
@@ -1351,7 +1357,7 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   }
   if (di->nitems) {
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(di->nitems, d.gemm_grid));
-    eval_dag<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+    eval_dag<false><<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
   }
   if (stage == 1)  // zeroes the counters for the next evaluation (stage 0 sets them itself)
     permute_out<<<pgrid, 256, 0, st>>>(d.yp, ldq, d.ipmap, Y, ldy, nn, qq, d.dag_done,

@@ -525,12 +525,15 @@ struct NoHook {
 // on S times as many SMs (the K loop of one tile is the DMMA time of one SM). Item `sub`
 // covers columns [sub 64/S, (sub+1) 64/S) of the block: its warps' fragments shift by that
 // many columns, and only 64/(16 S) fragment columns per warp are live.
-template <class WaitId, class KEnd = NoHook, class KStart = NoHook>
+// kNarrow (eval_dag's narrow instantiation): column-split items and the fused permutations'
+// final stores into Y. The wide instantiation keeps the tile loop of the round-1 kernel.
+template <bool kNarrow, class WaitId, class KEnd = NoHook, class KStart = NoHook>
 __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const CtaSmem& c, const RingSlot* rs,
                                                   const Task& task, std::uint32_t cb, const FragAddr& fa0,
                                                   std::uint32_t& it, WaitId&& wait_id, KEnd&& k_end = KEnd{},
                                                   KStart&& k_start = KStart{}, std::uint32_t sub = 0,
                                                   std::uint32_t split = 1) {
+  if (!kNarrow) sub = 0, split = 1;
   const std::uint32_t width = kBN / split, cs = sub * width;  // this item's columns in the block
   const std::uint32_t c0 = cb * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -624,14 +627,14 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
         case 2: consume_chunks<2, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         default: consume_chunks<1, 4>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
       }
-    } else if (live_j == 1 && split == 4) {  // column-split items: one live fragment column
+    } else if (kNarrow && live_j == 1 && split == 4) {  // column-split items: one live fragment column
       switch (live_i) {
         case 4: consume_chunks<4, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         case 3: consume_chunks<3, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         case 2: consume_chunks<2, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         default: consume_chunks<1, 1>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
       }
-    } else if (live_j == 2 && split == 2) {
+    } else if (kNarrow && live_j == 2 && split == 2) {
       switch (live_i) {
         case 4: consume_chunks<4, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
         case 3: consume_chunks<3, 2>(acc, c.full, c.empty, base, fa.a, fa.b, nch, lks, it); break;
@@ -648,7 +651,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
     add_rows(pick_buf(p, task.id_buf), pick_ld(p, task.id_buf), srcs, true);
   }
 
-  if (p.y_final && (task.flags & kTaskFinal)) {  // scattered into the caller's column-major Y
+  if (kNarrow && p.y_final && (task.flags & kTaskFinal)) {  // scattered into the caller's column-major Y
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int row = (2 * i + wm) * 8 + fr;
@@ -720,7 +723,7 @@ grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ 
       break;
     }
     const Task task = rs->task;
-    consume_gemm_tile(p, c, rs, task, static_cast<std::uint32_t>(t % col_blocks), fa, it,
+    consume_gemm_tile<false>(p, c, rs, task, static_cast<std::uint32_t>(t % col_blocks), fa, it,
                       [](const Task&, bool) {});  // the copied rows' level ran in an earlier launch
     release_item(c, seq);
   }
@@ -879,6 +882,10 @@ __device__ __forceinline__ void dag_exit(const DagParams& d) {
   if (threadIdx.x == 0) *d.exit_ctr = 0u;
 }
 
+// kNarrow: the instantiation for narrow DAGs (column-split items, padded counters, fused
+// permutations, self-reset); the wide one compiles those paths out (they cost the cfg5 DAG
+// 3.8% as runtime branches).
+template <bool kNarrow>
 __global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
 eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
          const __grid_constant__ CUtensorMap tm_s, const GemmParams p, const DagParams d) {
@@ -888,15 +895,15 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   pdl_trigger();  // permute_out may launch; it waits for this grid before reading Yp
   pdl_wait();     // Wp and the zeroed counters of permute_in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const std::uint64_t cst = d.cstride, region = static_cast<std::uint64_t>(d.nodes) * d.ncb * cst;
+  const std::uint64_t cst = kNarrow ? d.cstride : 1, region = static_cast<std::uint64_t>(d.nodes) * d.ncb * cst;
   std::uint32_t* const done_t = d.done;
   std::uint32_t* const done_s = done_t + region;
   std::uint32_t* const done_y = done_s + region;
   std::uint32_t* const done_w = done_y + region;
   auto at = [&](std::uint32_t node, std::uint32_t cb) { return (static_cast<std::uint64_t>(node) * d.ncb + cb) * cst; };
-  const std::uint32_t wmul = kConsumerWarps * d.colsplit;  // signals per complete row tile
+  const std::uint32_t wmul = kConsumerWarps * (kNarrow ? d.colsplit : 1);  // signals per complete row tile
 
-  if (d.fused && warp < kConsumerWarps) {
+  if (kNarrow && d.fused && warp < kConsumerWarps) {
     // Wp[ipmap[r]][phys(c)] = W[r + c ldw] in source order: a job is 32 consecutive points x
     // one column block, read as whole 256-byte column segments, transposed through shared
     // memory (the stage buffers: this CTA's producer issues no chunk before pbar) and written
@@ -978,7 +985,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         }
       };
       std::uint32_t it = 0;
-      bool stages_free = !d.fused;
+      bool stages_free = !kNarrow || !d.fused;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t q = atomicAdd(d.claim, 1u);
         const std::uint64_t item = q < d.nitems ? d.items[q] : make_item(kItemEnd, 0, 0);
@@ -999,7 +1006,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         }
         produce_gemm_tile(p, c, rs, cb, &tm_wp, &tm_t, &tm_s, it, [&](const SegDev& sg) {
           if (sg.bbuf == kBufWp) {
-            if (!d.fused) return;  // Wp is complete: permute_in ran before this launch
+            if (!kNarrow || !d.fused) return;  // Wp is complete: permute_in ran before this launch
             spin_until_svc(done_w + at(sg.src, cb), d.wp_target[sg.src], service);
           } else {
             spin_until_svc((sg.bbuf == kBufT ? done_t : done_s) + at(sg.src, cb),
@@ -1019,7 +1026,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         if (++polls > (1u << 26)) __trap();
       }
     }
-    dag_exit(d);
+    if (kNarrow) dag_exit(d);
     return;
   }
   // consumer warps: hand an item's stored tile (or, with kSigEnd, the end) to the producer
@@ -1047,7 +1054,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     if (stamp) HMXG_STAMP(seq, 3);
     const std::uint32_t cb = item_cb(item), sub = item_sub(item);
     const Task task = rs->task;
-    consume_gemm_tile(p, c, rs, task, cb, fa, it, [&](const Task& t, bool own_rows) {
+    consume_gemm_tile<kNarrow>(p, c, rs, task, cb, fa, it, [&](const Task& t, bool own_rows) {
       // the rows about to be read are complete for this column block (every lane acquires;
       // the reads are plain L2 loads): the near phase's rows of this leaf, or the nodes
       // whose rows are copied (Wp is complete before the launch)
@@ -1061,7 +1068,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         return;
       }
       if (t.id_buf == kBufWp) {
-        if (d.fused && t.id_node0 != kNoMap)
+        if (kNarrow && d.fused && t.id_node0 != kNoMap)
           wait_for(done_w + at(t.id_node0, cb), d.wp_target[t.id_node0]);
         return;
       }
@@ -1080,7 +1087,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
 #else
       (void)it0;
 #endif
-    }, sub, d.colsplit);
+    }, kNarrow ? sub : 0u, kNarrow ? d.colsplit : 1u);
     // Yp rows have a reader inside the launch only in the split leaf variant (the leaf
     // phase accumulates onto the near phase's rows of the same leaf)
     release_item(c, seq);
@@ -1093,7 +1100,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       warp_signal(ctr);
     if (stamp) HMXG_STAMP(seq, 5);
   }
-  dag_exit(d);
+  if (kNarrow) dag_exit(d);
 }
 
 // Race detector of debug runs (HMXG_POISON=1): every live row of a workspace buffer (the

@@ -45,7 +45,7 @@ def summary(lib: str) -> str:
         if "hmxg_cu" not in name:
             continue
         short = re.sub(r"_ZN4hmxg\d+_GLOBAL__N__\w+?_cu_\w+?\d+(\w+?)E.*", r"\1", name)
-        short = re.sub(r"^\d+", "", short)
+        short = re.sub(r"^\d+", "", short).replace("ILb0", "<false>").replace("ILb1", "<true>")
         out.append(f"{short:14s} {c['total']:6d}  " + "  ".join(f"{k}={c[k]}" for k in KEYS if c[k]))
         dm = {k: v for k, v in c.items() if k.startswith("DMMA.")}
         if dm:
