@@ -79,12 +79,20 @@ class Evaluator {
  public:
   explicit Evaluator(const hmx::CDS& cds, const std::vector<int>& devices = {0}) : n_(cds.tree.num_points()) {
     check(hmxg_create(devices.data(), static_cast<int>(devices.size()), &ctx_));
-    CdsView v(cds);
-    const int rc = hmxg_upload(ctx_, &v.view, &mat_);
-    if (rc != HMXG_OK) {
-      hmxg_destroy(ctx_);
-      raise(rc);
-    }
+    upload(cds);
+  }
+  // One process (or thread) per GPU with the caller's collective (hmxg_comm, include/hmxg.h).
+  // While the CDS fits comm.hbm_budget it is replicated and evaluate() is local (each rank
+  // passes its own columns). Otherwise this rank holds one subtree part (split() is true)
+  // and evaluate() is collective: every rank passes the same full W and gets the full Y.
+  Evaluator(const hmx::CDS& cds, int device, const hmxg_comm& comm) : n_(cds.tree.num_points()) {
+    check(hmxg_create_comm(device, &comm, &ctx_));
+    upload(cds);
+  }
+  bool split() const {
+    hmxg_info info{};
+    check(hmxg_info_get(mat_, &info));
+    return info.split_parts > 1;
   }
   Evaluator(const Evaluator&) = delete;
   Evaluator& operator=(const Evaluator&) = delete;
@@ -106,6 +114,14 @@ class Evaluator {
   }
 
  private:
+  void upload(const hmx::CDS& cds) {
+    CdsView v(cds);
+    const int rc = hmxg_upload(ctx_, &v.view, &mat_);
+    if (rc != HMXG_OK) {
+      hmxg_destroy(ctx_);
+      raise(rc);
+    }
+  }
   std::size_t n_ = 0;
   hmxg_ctx* ctx_ = nullptr;
   hmxg_mat* mat_ = nullptr;

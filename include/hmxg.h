@@ -109,6 +109,11 @@ typedef struct hmxg_info {
   uint64_t device_bytes;              /* resident generator + table bytes per device */
   double exec_flops_per_col;          /* flops the kernels execute per column (the bases'
                                          identity rows become row copies) */
+  uint32_t split_parts;               /* 1: the CDS is replicated on this device; P > 1: this
+                                         device holds one of P subtree parts (hmxg_create_comm
+                                         contexts whose CDS exceeds the HBM budget, or
+                                         hmxg_upload_split), and evaluation is collective */
+  uint32_t part;                      /* the part this device holds */
 } hmxg_info;
 
 /* One launch of the per-evaluation launch sequence (SURVEY §7.3 / DESIGN.md):
@@ -135,6 +140,36 @@ typedef struct hmxg_mat hmxg_mat;
 /* Context over `ndev` CUDA devices (devs may repeat a device id: each entry is one
  * column shard). ndev = 0 / devs = NULL means {0}. */
 int hmxg_create(const int* devs, int ndev, hmxg_ctx** out);
+
+/* ---- One process per GPU. The caller provides the collective:
+ * allgatherv(user, sendbuf, sendbytes, recvbuf, recvbytes[size], displs[size], stream):
+ * every rank contributes sendbytes bytes and receives rank r's block at recvbuf + displs[r]
+ * (recvbytes[r] bytes). The library always calls it in place (sendbuf == recvbuf +
+ * displs[rank]) on contiguous blocks in rank order. Buffers are device pointers ordered on
+ * `stream` (a cudaStream_t; e.g. ncclGroupStart + one ncclBroadcast per rank), or host
+ * memory with a NULL stream when host_buffers != 0 (the library stages; e.g. MPI, gloo).
+ * A non-zero return is reported as HMXG_ECOMM.
+ * hbm_budget: device bytes the resident CDS may use (0: 3/4 of the device's memory). While
+ * the CDS fits, hmxg_upload replicates it and every rank evaluates its own columns with no
+ * communication. When it does not, hmxg_upload holds only the rank's subtree part (the
+ * subtree-split fallback, hmxg_info.split_parts = size) and hmxg_evaluate becomes
+ * collective: every rank passes the same full W and receives the full Y; inside, the parts
+ * all-gather the skeleton weights T other parts read (children of the replicated top levels
+ * and far partners) and then their rows of the result. (Replaces the reference's in-process
+ * WorkerPool fork-join, /root/reference/proj/include/hmx/parallel.hpp:19-114, at process
+ * scale; the reference itself has no multi-process evaluation.) */
+typedef int (*hmxg_allgatherv_fn)(void* user, const void* sendbuf, size_t sendbytes, void* recvbuf,
+                                  const size_t* recvbytes, const size_t* displs, void* stream);
+typedef struct hmxg_comm {
+  uint32_t rank;
+  uint32_t size;
+  hmxg_allgatherv_fn allgatherv;
+  void* user;
+  int32_t host_buffers;
+  uint32_t reserved;
+  uint64_t hbm_budget;
+} hmxg_comm;
+int hmxg_create_comm(int dev, const hmxg_comm* comm, hmxg_ctx** out);
 int hmxg_destroy(hmxg_ctx* ctx);
 
 /* Validate the view, derive the level-batched task tables and copy the generators to

@@ -92,6 +92,27 @@ class Info(C.Structure):
         ("flops_per_col", C.c_double),
         ("device_bytes", C.c_uint64),
         ("exec_flops_per_col", C.c_double),
+        ("split_parts", C.c_uint32),
+        ("part", C.c_uint32),
+    ]
+
+
+# hmxg_allgatherv_fn (include/hmxg.h): user, sendbuf, sendbytes, recvbuf, recvbytes[], displs[], stream
+ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.POINTER(C.c_size_t),
+                            C.POINTER(C.c_size_t), C.c_void_p)
+
+
+class Comm(C.Structure):
+    """``hmxg_comm``."""
+
+    _fields_ = [
+        ("rank", C.c_uint32),
+        ("size", C.c_uint32),
+        ("allgatherv", ALLGATHERV_FN),
+        ("user", C.c_void_p),
+        ("host_buffers", C.c_int32),
+        ("reserved", C.c_uint32),
+        ("hbm_budget", C.c_uint64),
     ]
 
 
@@ -164,6 +185,7 @@ class BuildStats(C.Structure):
 HMXG_SYMBOLS = {
     "hmxg_create": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]),
     "hmxg_destroy": (C.c_int, [C.c_void_p]),
+    "hmxg_create_comm": (C.c_int, [C.c_int, C.POINTER(Comm), C.POINTER(C.c_void_p)]),
     "hmxg_upload": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.POINTER(C.c_void_p)]),
     "hmxg_free": (C.c_int, [C.c_void_p]),
     "hmxg_validate": (C.c_int, [C.POINTER(CdsView), C.POINTER(Info)]),

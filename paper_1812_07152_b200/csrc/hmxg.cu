@@ -100,6 +100,9 @@ struct DevState {
   std::uint32_t* yp_tiles = nullptr;
   // fused permutations (small problems, see fused_io): padded row -> point, and the leaf jobs
   std::uint32_t* pmap = nullptr;
+  // host staging of host-buffer collectives (hmxg_comm::host_buffers)
+  unsigned char* comm_host = nullptr;
+  std::size_t comm_host_bytes = 0;
   std::uint32_t* rowleaf = nullptr;    // Wp row -> leaf node
   std::uint32_t* wp_target = nullptr;  // leaf node -> rows
   // an enqueue failed between eval_dag and the launch that zeroes its counters: zero them first
@@ -196,6 +199,9 @@ struct DevState {
     pmap = nullptr;
     cudaFree(rowleaf);
     rowleaf = nullptr;
+    cudaFreeHost(comm_host);
+    comm_host = nullptr;
+    comm_host_bytes = 0;
     cudaFree(wp_target);
     wp_target = nullptr;
     dag_done = nullptr;
@@ -1035,6 +1041,147 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
   return HMXG_OK;
 }
 
+// The caller's collective over contiguous row blocks [row[r], row[r + 1]) of a point-major
+// buffer (row pitch ld doubles), in place; HMXG_ECOMM when it fails.
+int comm_allgather_rows(const hmxg_comm& cm, DevState& d, double* base, std::uint64_t ld,
+                        const std::vector<std::uint64_t>& row, cudaStream_t st) {
+  const std::size_t P = cm.size, rb = ld * sizeof(double);
+  std::vector<std::size_t> counts(P), displs(P);
+  for (std::size_t r = 0; r < P; ++r) {
+    displs[r] = row[r] * rb;
+    counts[r] = (row[r + 1] - row[r]) * rb;
+  }
+  const std::size_t total = row[P] * rb;
+  if (total == 0) return HMXG_OK;
+  int rc = 0;
+  if (cm.host_buffers) {
+    if (total > d.comm_host_bytes) {
+      cudaFreeHost(d.comm_host);
+      d.comm_host = nullptr;
+      d.comm_host_bytes = 0;
+      HMXG_CUDA(cudaHostAlloc(&d.comm_host, total, cudaHostAllocPortable));
+      d.comm_host_bytes = total;
+    }
+    unsigned char* dev = reinterpret_cast<unsigned char*>(base);
+    const std::size_t me = cm.rank;
+    if (counts[me]) HMXG_CUDA(cudaMemcpyAsync(d.comm_host + displs[me], dev + displs[me], counts[me], cudaMemcpyDeviceToHost, st));
+    HMXG_CUDA(cudaStreamSynchronize(st));
+    rc = cm.allgatherv(cm.user, d.comm_host + displs[me], counts[me], d.comm_host, counts.data(), displs.data(), nullptr);
+    if (rc == 0) HMXG_CUDA(cudaMemcpyAsync(dev, d.comm_host, total, cudaMemcpyHostToDevice, st));
+  } else {
+    unsigned char* dev = reinterpret_cast<unsigned char*>(base);
+    rc = cm.allgatherv(cm.user, dev + displs[cm.rank], counts[cm.rank], dev, counts.data(), displs.data(), st);
+  }
+  if (rc != 0) return set_err(HMXG_ECOMM, "hmxg_evaluate: allgatherv failed (" + std::to_string(rc) + ")");
+  return HMXG_OK;
+}
+
+// Collective evaluation of a subtree-split matrix (hmxg_create_comm, CDS over the HBM
+// budget): every rank passes the same full W. Stage 0 runs the upward pass over the rank's
+// subtrees; the ranks all-gather the T rows other parts read (Plan::pub_row); stage 1 runs
+// the replicated top levels, far+downward and the near/leaf rows of the rank's leaves; the
+// ranks all-gather their Yp rows (Plan::yp_row) and every rank permutes out the full Y.
+int split_evaluate(hmxg_mat* mat, const double* W, std::size_t ldw, double* Y, std::size_t ldy, std::size_t q,
+                   unsigned flags, void* stream, std::uint32_t* launches) {
+  const Plan& plan = mat->plan;
+  const hmxg_comm& cm = mat->ctx->comm;
+  if (cm.size != plan.nparts || cm.rank != plan.part)
+    return set_err(HMXG_EINVAL, "hmxg_evaluate: a split matrix evaluates through its hmxg_create_comm context "
+                                "(or stage by stage with hmxg_split_stage)");
+  DevState& d = mat->devs[0];
+  HMXG_CUDA(cudaSetDevice(d.dev));
+  const bool dev_ptrs = flags & HMXG_F_DEVICE_PTRS;
+  cudaStream_t st = dev_ptrs && stream ? static_cast<cudaStream_t>(stream) : d.comp;
+  const std::size_t n = plan.n;
+  const double* Wd = W;
+  double* Yd = Y;
+  std::size_t ldwd = ldw, ldyd = ldy;
+  HMXG_TRY(ensure_workspace(plan, d, q));
+  if (!dev_ptrs) {
+    HMXG_TRY(ensure_stage(plan, d, q));
+    HMXG_TRY(copy_cols(d.w_stage[0], n, W, ldw, n, q, cudaMemcpyHostToDevice, st));
+    Wd = d.w_stage[0];
+    Yd = d.y_stage[0];
+    ldwd = ldyd = n;
+  }
+  const DevState::DagItems* di[2] = {nullptr, nullptr};
+  for (std::uint32_t stage = 0; stage < 2; ++stage) HMXG_TRY(ensure_dag(plan, d, q, st, &di[stage], stage));
+  HMXG_TRY(order_after_previous(d, st));
+  const std::uint32_t qq = static_cast<std::uint32_t>(q), nn = static_cast<std::uint32_t>(n);
+  const std::uint64_t ldq = d.cap_q;
+  const std::uint32_t ncb = (qq + kBN - 1) / kBN;
+  const std::size_t words = dag_done_words(plan, q);
+  CUtensorMap tm_wp, tm_t, tm_s;
+  HMXG_TRY(make_map(&tm_wp, d.wp, plan.rows_pad, q, ldq));
+  HMXG_TRY(make_map(&tm_t, d.t, plan.skel_rows, q, ldq));
+  HMXG_TRY(make_map(&tm_s, d.s, plan.skel_rows, q, ldq));
+  GemmParams p{};
+  p.tiles = d.tiles;
+  p.tasks = d.tasks;
+  p.segs = d.segs;
+  p.idmap = d.idmap;
+  p.buf[kBufWp] = d.wp;
+  p.buf[kBufT] = d.t;
+  p.buf[kBufS] = d.s;
+  p.buf[kBufYp] = d.yp;
+  for (auto& l : p.ld) l = ldq;
+  p.q = qq;
+  const dim3 pgrid((nn + kTT - 1) / kTT, (qq + kTT - 1) / kTT);
+  if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
+  d.counters_dirty = true;
+  HMXG_CUDA(cudaMemsetAsync(d.t, 0, plan.skel_rows * ldq * sizeof(double), st));
+  HMXG_CUDA(cudaMemsetAsync(d.yp, 0, plan.rows_pad * ldq * sizeof(double), st));
+  HMXG_CUDA(cudaMemsetAsync(d.dag_done, 0, (words + 1) * sizeof(std::uint32_t), st));
+  permute_in<<<pgrid, 256, 0, st>>>(Wd, ldwd, d.ipmap, d.wp, ldq, nn, qq, nullptr, 0);
+  ++*launches;
+  for (std::uint32_t stage = 0; stage < 2; ++stage) {
+    DagParams dp{};
+    dp.items = di[stage]->items;
+    dp.nitems = di[stage]->nitems;
+    dp.claim = d.dag_done + stage;
+    dp.done = d.dag_done + kDagClaimWords;
+    dp.node_tiles = d.node_tiles;
+    dp.yp_tiles = d.yp_tiles;
+    dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
+    dp.colsplit = 1;
+    dp.cstride = 1;
+    dp.ncb = ncb;
+    dp.nodes = plan.num_nodes;
+    dp.fwd_signals = forward_signals(di[stage]->nitems, d.gemm_grid);
+    if (stage == 1) {
+      // the T rows other parts publish, then their completion for stage 1's waits
+      HMXG_TRY(comm_allgather_rows(cm, d, d.t, ldq, plan.pub_row, st));
+      if (!plan.remote_t_nodes.empty()) {
+        const std::uint64_t cells = std::uint64_t(plan.remote_t_nodes.size()) * ncb;
+        preset_done<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, st>>>(
+            d.remote_t, static_cast<std::uint32_t>(plan.remote_t_nodes.size()), dp.done, ncb, d.node_tiles);
+        ++*launches;
+      }
+    }
+    if (dp.nitems) {
+      const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(dp.nitems, d.gemm_grid));
+      eval_dag<false><<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+      ++*launches;
+    }
+  }
+  HMXG_TRY(comm_allgather_rows(cm, d, d.yp, ldq, plan.yp_row, st));  // every part's result rows
+  permute_out<<<pgrid, 256, 0, st>>>(d.yp, ldq, d.ipmap, Yd, ldyd, nn, qq, d.dag_done, words + 1);
+  ++*launches;
+  HMXG_CUDA(cudaGetLastError());
+  d.counters_dirty = false;
+  d.last_fused = false;
+  d.last_launches = *launches;
+  if (!dev_ptrs) HMXG_TRY(copy_cols(Y, ldy, d.y_stage[0], n, n, q, cudaMemcpyDeviceToHost, st));
+  if (!dev_ptrs || !(flags & HMXG_F_NO_SYNC)) {
+    HMXG_CUDA(cudaStreamSynchronize(st));
+    d.pending = false;
+  } else {
+    HMXG_CUDA(cudaEventRecord(d.ev_last, st));
+    d.pending = true;
+  }
+  return HMXG_OK;
+}
+
 }  // namespace
 }  // namespace hmxg
 
@@ -1068,6 +1215,18 @@ int hmxg_create(const int* devs, int ndev, hmxg_ctx** out) {
     if (prop.major != 10) return set_err(HMXG_ECUDA, "hmxg_create: built for sm_100a (B200) only");
   }
   *out = ctx.release();
+  return HMXG_OK;
+}
+
+int hmxg_create_comm(int dev, const hmxg_comm* comm, hmxg_ctx** out) {
+  if (!out || !comm) return set_err(HMXG_EINVAL, "hmxg_create_comm: null argument");
+  *out = nullptr;
+  if (comm->size == 0 || comm->rank >= comm->size) return set_err(HMXG_EINVAL, "hmxg_create_comm: bad rank / size");
+  if (comm->size > 1 && !comm->allgatherv) return set_err(HMXG_EINVAL, "hmxg_create_comm: no allgatherv");
+  hmxg_ctx* ctx = nullptr;
+  HMXG_TRY(hmxg_create(&dev, 1, &ctx));
+  ctx->comm = *comm;
+  *out = ctx;
   return HMXG_OK;
 }
 
@@ -1249,6 +1408,23 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
 }
 
 int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
+  if (ctx && cds && ctx->comm.size > 1) {
+    // one process per GPU: replicate while the resident CDS fits the budget, else hold this
+    // rank's subtree part (SURVEY §8e fallback)
+    Plan probe;
+    std::string err;
+    if (!build_plan(*cds, kBM, probe, err)) return set_err(HMXG_EINVAL, err);
+    const std::uint64_t bytes = 8 * probe.tile_elems + sizeof(Task) * probe.tasks.size() +
+                                sizeof(SegDev) * probe.segs.size() + 4 * (probe.ipmap.size() + probe.idmap.size());
+    std::uint64_t budget = ctx->comm.hbm_budget;
+    if (budget == 0) {
+      std::size_t free_b = 0, total_b = 0;
+      HMXG_CUDA(cudaSetDevice(ctx->devs[0]));
+      HMXG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      budget = total_b / 4 * 3;
+    }
+    if (bytes > budget) return upload_impl(ctx, cds, SplitSpec{ctx->comm.size, ctx->comm.rank}, out);
+  }
   return upload_impl(ctx, cds, SplitSpec{}, out);
 }
 
@@ -1411,6 +1587,8 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   info->flops_per_col = 2.0 * (2.0 * p.v_elems + p.b_elems + p.d_elems);
   for (const Phase& ph : p.phases) info->exec_flops_per_col += ph.flops_per_col;
   info->device_bytes = mat->devs.empty() ? 0 : mat->devs[0].resident_bytes;
+  info->split_parts = p.nparts;
+  info->part = p.part;
   return HMXG_OK;
 }
 
@@ -1490,7 +1668,9 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
   std::uint32_t launches = 0;
   float dev_ms = 0.f;
 
-  if (flags & HMXG_F_DEVICE_PTRS) {
+  if (plan.nparts > 1) {  // subtree-split part: a collective evaluation (hmxg_create_comm)
+    HMXG_TRY(split_evaluate(mat, W, ldw, Y, ldy, q, flags, stream, &launches));
+  } else if (flags & HMXG_F_DEVICE_PTRS) {
     if (mat->devs.size() != 1)
       return set_err(HMXG_EINVAL, "hmxg_evaluate: device pointers need a single-device context");
     DevState& d = mat->devs[0];

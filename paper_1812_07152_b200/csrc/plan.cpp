@@ -190,13 +190,82 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       plan.pmap[plan.leaf_row[i] + r] = orig;
       plan.ipmap[orig] = static_cast<std::uint32_t>(plan.leaf_row[i] + r);
     }
+  // --- subtree split: owner part of every node (-1: replicated top level)
+  if (split.nparts == 0 || split.part >= split.nparts) return fail(err, "split: bad part / nparts");
+  plan.nparts = split.nparts;
+  plan.part = split.part;
+  const bool splitting = split.nparts > 1;
+  std::vector<int> owner(nn, 0);
+  if (splitting) {
+    std::uint32_t top_depth = 0;
+    while ((1u << top_depth) < split.nparts) ++top_depth;
+    std::vector<std::uint32_t> roots;  // subtree roots in tree-position order
+    for (std::uint32_t i : order)
+      if (v.level[i] == top_depth || (v.level[i] < top_depth && is_leaf(i))) roots.push_back(i);
+    std::sort(roots.begin(), roots.end(), [&](std::uint32_t a, std::uint32_t b) { return v.start[a] < v.start[b]; });
+    for (std::uint32_t i = 0; i < nn; ++i) owner[i] = -1;
+    for (std::size_t k = 0; k < roots.size(); ++k)
+      owner[roots[k]] = static_cast<int>(k * split.nparts / roots.size());
+    for (std::uint32_t i : order)  // BFS: parents before children
+      if (!is_leaf(i) && owner[i] >= 0) owner[v.lchild[i]] = owner[v.rchild[i]] = owner[i];
+    for (std::uint32_t i = 0; i < nn; ++i)
+      if (owner[i] >= 0 && owner[i] != static_cast<int>(split.part) && active(i)) plan.remote_t_nodes.push_back(i);
+  }
+  // Split mode: the T rows a part publishes (the nodes another part's stage 1 reads: children
+  // of the replicated top nodes, and far partners of top nodes or of another part's nodes)
+  // come first in T, grouped by part, so the exchange is one in-place all-gather of
+  // contiguous row ranges (pub_row[p], pub_row[p + 1]) instead of a sum over the whole T.
+  // Each part's leaves are contiguous in Wp / Yp: the result rows of part p are
+  // [yp_row[p], yp_row[p + 1]).
+  std::vector<std::uint8_t> published(nn, 0);
+  if (splitting) {
+    for (std::uint32_t i = 0; i < nn; ++i) {
+      if (owner[i] < 0 || !active(i)) continue;
+      const std::uint32_t par = v.parent[i];
+      if (par != HMXG_NO_NODE && owner[par] < 0) published[i] = 1;
+    }
+    for (std::uint32_t c = 0; c < nn; ++c)
+      for (std::uint64_t s : far_of[c]) {
+        const std::uint32_t j = v.far_pairs[2 * s + 1];
+        if (owner[j] >= 0 && (owner[c] < 0 || owner[c] != owner[j])) published[j] = 1;
+      }
+  }
   plan.node_off.assign(nn, 0);
   std::uint64_t rows = 0;
+  plan.pub_row.assign(split.nparts + 1, 0);
+  if (splitting) {
+    for (std::uint32_t p = 0; p < split.nparts; ++p) {
+      plan.pub_row[p] = rows;
+      for (std::uint32_t i : order)
+        if (published[i] && owner[i] == static_cast<int>(p)) {
+          plan.node_off[i] = rows;
+          rows += pad16(v.sranks[i]);
+        }
+    }
+    plan.pub_row[split.nparts] = rows;
+  }
   for (std::uint32_t i : order)
-    if (active(i)) {
+    if (active(i) && !published[i]) {
       plan.node_off[i] = rows;
       rows += pad16(v.sranks[i]);
     }
+  plan.yp_row.assign(split.nparts + 1, 0);
+  if (splitting) {
+    std::vector<std::uint64_t> lo(split.nparts, ~std::uint64_t(0)), hi(split.nparts, 0), cnt(split.nparts, 0);
+    for (std::uint32_t i : leaves_by_start) {
+      const int o = owner[i];
+      if (o < 0) return fail(err, "split: leaf without an owner part");
+      lo[o] = std::min(lo[o], plan.leaf_row[i]);
+      hi[o] = std::max(hi[o], plan.leaf_row[i] + pad16(size_of(i)));
+      cnt[o] += pad16(size_of(i));
+    }
+    for (std::uint32_t p = 0; p < split.nparts; ++p) {
+      if (cnt[p] == 0) lo[p] = hi[p] = p ? plan.yp_row[p] : 0;
+      if (hi[p] - lo[p] != cnt[p] || lo[p] != (p ? plan.yp_row[p] : 0))
+        return fail(err, "split: the leaves of part ", p, " are not contiguous");
+      plan.yp_row[p + 1] = hi[p];
+    }
+  }
   if (rows > std::numeric_limits<std::uint32_t>::max() - kRowAlign) return fail(err, "cds: too many skeleton rows");
   plan.skel_rows = std::max<std::uint64_t>(rows, kRowAlign);
 
@@ -276,27 +345,6 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
     plan.tile_src.push_back(ts);
     plan.tile_elems += chunks * kRowAlign * bm;
   };
-  // --- subtree split: owner part of every node (-1: replicated top level)
-  if (split.nparts == 0 || split.part >= split.nparts) return fail(err, "split: bad part / nparts");
-  plan.nparts = split.nparts;
-  plan.part = split.part;
-  const bool splitting = split.nparts > 1;
-  std::vector<int> owner(nn, 0);
-  if (splitting) {
-    std::uint32_t top_depth = 0;
-    while ((1u << top_depth) < split.nparts) ++top_depth;
-    std::vector<std::uint32_t> roots;  // subtree roots in tree-position order
-    for (std::uint32_t i : order)
-      if (v.level[i] == top_depth || (v.level[i] < top_depth && is_leaf(i))) roots.push_back(i);
-    std::sort(roots.begin(), roots.end(), [&](std::uint32_t a, std::uint32_t b) { return v.start[a] < v.start[b]; });
-    for (std::uint32_t i = 0; i < nn; ++i) owner[i] = -1;
-    for (std::size_t k = 0; k < roots.size(); ++k)
-      owner[roots[k]] = static_cast<int>(k * split.nparts / roots.size());
-    for (std::uint32_t i : order)  // BFS: parents before children
-      if (!is_leaf(i) && owner[i] >= 0) owner[v.lchild[i]] = owner[v.rchild[i]] = owner[i];
-    for (std::uint32_t i = 0; i < nn; ++i)
-      if (owner[i] >= 0 && owner[i] != static_cast<int>(split.part) && active(i)) plan.remote_t_nodes.push_back(i);
-  }
   const int me = static_cast<int>(split.part);
   auto mine = [&](std::uint32_t i) { return !splitting || owner[i] == me; };
   auto top = [&](std::uint32_t i) { return splitting && owner[i] < 0; };

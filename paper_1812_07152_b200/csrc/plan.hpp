@@ -150,6 +150,8 @@ struct Plan {
   // subtree-split mode (SURVEY §8e fallback): nodes whose T arrives through the exchange
   std::uint32_t nparts = 1, part = 0;
   std::vector<std::uint32_t> remote_t_nodes;
+  std::vector<std::uint64_t> pub_row;     // nparts + 1: T rows each part publishes (in place)
+  std::vector<std::uint64_t> yp_row;      // nparts + 1: Wp / Yp rows of each part's leaves
   std::uint32_t leaf_tasks = 0;           // row tiles of the leaf (Yp) phase
   std::uint64_t d_elems = 0, b_elems = 0, v_elems = 0;
   std::uint32_t max_m = 0;

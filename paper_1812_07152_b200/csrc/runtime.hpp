@@ -14,6 +14,7 @@
 
 struct hmxg_ctx {
   std::vector<int> devs;
+  hmxg_comm comm{};  // size 0: no communicator (hmxg_create)
 };
 
 namespace hmxg {

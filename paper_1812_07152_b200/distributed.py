@@ -169,3 +169,69 @@ def split_evaluate(cds: CDS, w, parts: list["SplitPart"] | None = None, nparts: 
     for part, y in zip(parts, ys):
         part.stage(1, w.data_ptr(), y.data_ptr(), q, stream=st)
     return allreduce(torch.stack(ys).sum(0) if len(ys) > 1 else ys[0])
+
+
+class _DeviceBytes:
+    """A device byte range as a torch tensor (``__cuda_array_interface__``, no copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+
+class TorchComm:
+    """``hmxg_comm`` over a ``torch.distributed`` process group (one process per GPU).
+
+    The C-ABI calls ``allgatherv`` in place on contiguous blocks in rank order. With NCCL the
+    blocks stay on the device and every rank's block is broadcast from its owner on the
+    library's stream; with any other backend (gloo) the library stages through pinned host
+    memory (``host_buffers``) and the blocks travel as padded byte tensors. A failure returns
+    non-zero, which the library reports as HMXG_ECOMM.
+    ``hbm_budget``: bytes the resident CDS may use per device before ``hmxg_upload`` falls back
+    to the subtree split (0: 3/4 of the device's memory).
+    """
+
+    def __init__(self, group=None, hbm_budget: int = 0, host_buffers: bool | None = None):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        self.host_buffers = (backend != "nccl") if host_buffers is None else bool(host_buffers)
+        self.errors: list[str] = []
+        self._fn = N.ALLGATHERV_FN(self._allgatherv)  # kept alive with the struct
+        self.struct = N.Comm(rank=self.rank, size=self.size, allgatherv=self._fn, user=None,
+                             host_buffers=1 if self.host_buffers else 0, reserved=0, hbm_budget=int(hbm_budget))
+        self._C = C
+
+    def _allgatherv(self, user, send, sendbytes, recv, recvbytes, displs, stream):
+        import torch
+        import torch.distributed as dist
+
+        C = self._C
+        try:
+            counts = [int(recvbytes[r]) for r in range(self.size)]
+            disp = [int(displs[r]) for r in range(self.size)]
+            if self.host_buffers:
+                m = max(counts) or 1
+                mine = torch.zeros(m, dtype=torch.uint8)
+                if sendbytes:
+                    C.memmove(mine.data_ptr(), send, sendbytes)
+                outs = [torch.empty(m, dtype=torch.uint8) for _ in range(self.size)]
+                dist.all_gather(outs, mine, group=self.group)
+                for r in range(self.size):
+                    if counts[r]:
+                        C.memmove(recv + disp[r], outs[r].data_ptr(), counts[r])
+            else:
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+                    for r in range(self.size):
+                        if counts[r]:
+                            t = torch.as_tensor(_DeviceBytes(recv + disp[r], counts[r]), device="cuda")
+                            dist.broadcast(t, src=dist.get_global_rank(self.group, r) if self.group else r,
+                                           group=self.group)
+            return 0
+        except Exception as e:  # reported by the library as HMXG_ECOMM
+            self.errors.append(repr(e))
+            return 1

@@ -121,12 +121,19 @@ def plan_pseudocode(plan: EvalPlan | None = None) -> str:
 class Context:
     """``hmxg_ctx`` over device ids (repeats allowed: one column shard per entry)."""
 
-    def __init__(self, devices=(0,)):
+    def __init__(self, devices=(0,), comm=None):
+        """``comm`` (a distributed.TorchComm): one process per GPU (hmxg_create_comm) on
+        ``devices[0]``; uploads then replicate the CDS while it fits the comm's HBM budget and
+        hold this rank's subtree part otherwise (evaluation is then collective)."""
         lib = N.hmxg()
-        devs = (C.c_int * len(devices))(*devices)
         h = C.c_void_p()
-        _check(lib.hmxg_create(devs, len(devices), C.byref(h)))
+        if comm is not None:
+            _check(lib.hmxg_create_comm(int(devices[0]), C.byref(comm.struct), C.byref(h)))
+        else:
+            devs = (C.c_int * len(devices))(*devices)
+            _check(lib.hmxg_create(devs, len(devices), C.byref(h)))
         self._h = h
+        self.comm = comm  # the collective's callback must outlive the context
         self.devices = tuple(devices)
 
     @property

@@ -19,3 +19,17 @@ def test_reference_executor_suite_through_shim():
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "checks passed" in out.stdout
+
+
+SPLIT_BIN = os.path.join(ROOT, "oracle", "_ref", "test_split_gpu")
+
+
+@pytest.mark.skipif(not os.path.exists(SPLIT_BIN), reason="oracle/_ref/test_split_gpu not built")
+def test_subtree_split_fallback_through_shim():
+    """hmx_gpu::Evaluator(cds, device, hmxg_comm) with an HBM budget the CDS exceeds: two
+    ranks hold one subtree part each and evaluate collectively, bit-identical to the
+    replicated evaluation; a failing collective is HMXG_ECOMM (tests/cpp/test_split_gpu.cpp)."""
+    out = subprocess.run([SPLIT_BIN], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "split checks passed" in out.stdout
