@@ -91,6 +91,7 @@ struct DevState {
     std::uint64_t* items = nullptr;
     std::uint32_t nitems = 0;
     std::uint32_t stage = 0;
+    bool ct = false;  // CTree mode (near tiles only): the mode can change with the environment
   };
   DagItems dag[4];                    // item lists of the last few (column count, stage) keys
   std::uint32_t dag_next = 0;
@@ -103,6 +104,14 @@ struct DevState {
   // host staging of host-buffer collectives (hmxg_comm::host_buffers)
   unsigned char* comm_host = nullptr;
   std::size_t comm_host_bytes = 0;
+  // CTree program (ctree_csize): work units by level, built on first use
+  unsigned char* ct_blob = nullptr;  // tasks, then segments at ct_segs_off
+  std::uint32_t* ct_units = nullptr;
+  std::uint32_t* ct_lvl = nullptr;
+  std::uint32_t ct_nlev = 0, ct_blob_bytes = 0, ct_segs_off = 0;
+  std::uint64_t ct_tile_base = 0, ct_tile_lines = 0;
+  int ct_occ_c = 0;          // cluster size of the cached occupancy
+  unsigned ct_occ_ctas = 0;  // resident CTAs of eval_dag<true> in clusters of ct_occ_c
   std::uint32_t* rowleaf = nullptr;    // Wp row -> leaf node
   std::uint32_t* wp_target = nullptr;  // leaf node -> rows
   // an enqueue failed between eval_dag and the launch that zeroes its counters: zero them first
@@ -199,6 +208,12 @@ struct DevState {
     pmap = nullptr;
     cudaFree(rowleaf);
     rowleaf = nullptr;
+    cudaFree(ct_units);
+    cudaFree(ct_lvl);
+    cudaFree(ct_blob);
+    ct_units = ct_lvl = nullptr;
+    ct_blob = nullptr;
+    ct_nlev = 0;
     cudaFreeHost(comm_host);
     comm_host = nullptr;
     comm_host_bytes = 0;
@@ -287,8 +302,10 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 #ifndef HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA
 #define HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA 48
 #endif
+std::uint32_t ctree_csize(const Plan& plan, std::size_t q, unsigned grid);
 bool split_leaf(const Plan& plan, std::size_t q, unsigned grid) {
   if (plan.split_phases.empty()) return false;
+  if (ctree_csize(plan, q, grid)) return true;  // the CTree's leaf rows accumulate onto the near tiles
   std::uint64_t tasks = 0;
   for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
   return tasks * ((q + kBN - 1) / kBN) < std::uint64_t(HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA) * grid;
@@ -329,6 +346,11 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
         for (std::uint32_t sub = 0; sub < S; ++sub) items.push_back(make_item(kItemGemm, cb, t, sub));
   };
   const bool split = split_leaf(plan, q, grid);
+  if (stage == 0 && ctree_csize(plan, q, grid)) {  // CTree mode: the near tiles only
+    for (const Phase& ph : plan.split_phases)
+      if (ph.kind == kPhaseNear) emit(ph.task_begin, ph.task_end);
+    return items;
+  }
   std::vector<const Phase*> tree, leaf;
   const Phase* near = nullptr;
   for (const Phase& ph : plan.phases) {
@@ -400,11 +422,86 @@ bool fused_io(const Plan& plan, std::size_t q) {
   return plan.nparts == 1 && plan.n * q <= std::uint64_t(HMXG_FUSED_MAX_ELEMS) && std::getenv("HMXG_NO_FUSED") == nullptr;
 }
 
+// CTree mode (kernels.cuh, ct_run; opt-in with HMXG_CTREE=1): small fused problems whose tree
+// work per 8-column octet is small run every task but the near field in clusters of CTAs, one
+// cluster per octet, level by level with cluster barriers, instead of through the DAG's
+// gpu-scope counters (~4 us per dependent level on cfg1). The tasks are the upward and
+// far+downward phases and the split variant's accumulating leaf phase (ct_levels); the work
+// bound is DMMAs per octet. Bit-identical to the DAG, but measured slower on cfg1 (115 vs 55
+// us): an 8-column unit does ~30 instructions of operand addressing per
+// DMMA and waits ~0.8 us per 3-k-step block. Returns the cluster size (0: the DAG runs every
+// task); HMXG_CT_CLUSTER sets the size.
+#ifndef HMXG_CT_MAX_DMMA_PER_OCTET
+#define HMXG_CT_MAX_DMMA_PER_OCTET 16384
+#endif
+std::vector<const Phase*> ct_levels(const Plan& plan) {
+  std::vector<const Phase*> lv;
+  for (const Phase& ph : plan.phases)
+    if (ph.stage == 0 && ph.kind != kPhaseLeaf) lv.push_back(&ph);
+  for (const Phase& ph : plan.split_phases)
+    if (ph.stage == 0 && ph.kind != kPhaseNear) lv.push_back(&ph);
+  return lv;
+}
+double ct_dmma_per_octet(const Plan& plan) {
+  double n = 0.0;
+  std::uint64_t tasks = 0, steps = 0;
+  for (const Phase* ph : ct_levels(plan))
+    for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {
+      const Task& tk = plan.tasks[t];
+      ++tasks;
+      for (std::uint32_t r0 = 0; r0 < tk.m; r0 += 8)
+        for (std::uint32_t si = tk.seg_begin; si < tk.seg_end; ++si) {
+          const SegDev& sg = plan.segs[si];
+          if ((sg.rows && r0 >= sg.rows) || sg.nchunks == 0) continue;
+          n += 4.0 * (sg.nchunks - 1) + (sg.last_ksteps ? sg.last_ksteps : 4);
+        }
+      for (std::uint32_t si = tk.seg_begin; si < tk.seg_end; ++si) {
+        const SegDev& sg = plan.segs[si];
+        if (sg.nchunks) steps += 4u * (sg.nchunks - 1u) + (sg.last_ksteps ? sg.last_ksteps : 4u);
+      }
+    }
+  plan.ct_smem = (tasks * sizeof(Task) + 15) / 16 * 16 + (steps * sizeof(CtStep) + 15) / 16 * 16;
+  return tasks ? n : 1e300;  // no tree tasks: nothing for a CTree
+}
+std::uint32_t ctree_csize(const Plan& plan, std::size_t q, unsigned grid) {
+  if (!fused_io(plan, q) || plan.split_phases.empty() || !std::getenv("HMXG_CTREE")) return 0;
+  if (plan.ct_dmma < 0.0) plan.ct_dmma = ct_dmma_per_octet(plan);
+  if (plan.ct_dmma > HMXG_CT_MAX_DMMA_PER_OCTET || plan.ct_smem > std::uint64_t(kStages) * kStageBytes) return 0;
+  const std::size_t noct = (q + 7) / 8;
+  std::uint32_t c = 4;
+  if (const char* e = std::getenv("HMXG_CT_CLUSTER")) c = static_cast<std::uint32_t>(std::max(1, std::min(8, std::atoi(e))));
+  while (c > 1 && noct * c * 2 > grid) c /= 2;  // at most half of the grid in CTree clusters
+  return noct * c * 2 <= grid ? c : 0u;
+}
+
+// Resident CTAs of eval_dag<true> launched in clusters of c (cached per c).
+int ct_resident(DevState& d, std::uint32_t c) {
+  if (d.ct_occ_c == static_cast<int>(c)) return HMXG_OK;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(d.gemm_grid - d.gemm_grid % c);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = c;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  HMXG_CUDA(cudaOccupancyMaxActiveClusters(&clusters, eval_dag<true>, &cfg));
+  if (clusters <= 0) return set_err(HMXG_ECUDA, "eval_dag: no cluster of the CTree size fits an SM group");
+  d.ct_occ_c = static_cast<int>(c);
+  d.ct_occ_ctas = std::min<unsigned>(d.gemm_grid, static_cast<unsigned>(clusters) * c);
+  return HMXG_OK;
+}
+
 // Item list and counters for q columns (built on first use, cached for a few q).
 int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, const DevState::DagItems** out,
                std::uint32_t stage = 0) {
+  const bool ct = stage == 0 && ctree_csize(plan, q, d.gemm_grid) != 0;
   for (const auto& e : d.dag)
-    if (e.items && e.q == q && e.stage == stage) {
+    if (e.items && e.q == q && e.stage == stage && e.ct == ct) {
       *out = &e;
       return HMXG_OK;
     }
@@ -431,10 +528,65 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
     d.dag_done_cap = words;
     d.counters_dirty = false;
   }
+  if (stage == 0 && ctree_csize(plan, q, d.gemm_grid) && !d.ct_units) {
+    // CTree program: its tasks in level order, each with the flat list of its k steps in the
+    // DAG's order (kernels.cuh CtStep), in one blob; (local task << 5 | first octet) units of
+    // kCtG row octets, level by level; the range of A chunks they read
+    std::vector<Task> tasks;
+    std::vector<CtStep> steps;
+    std::vector<std::uint32_t> units, lvl{0};
+    std::uint64_t t_lo = ~0ull, t_hi = 0;
+    for (const Phase* ph : ct_levels(plan)) {
+      for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {
+        Task tk = plan.tasks[t];
+        const std::uint32_t kb = static_cast<std::uint32_t>(steps.size());
+        std::uint32_t wp_leaf = kNoMap;
+        for (std::uint32_t si = tk.seg_begin; si < tk.seg_end; ++si) {
+          const SegDev& sg = plan.segs[si];
+          if (sg.nchunks == 0) continue;
+          if (sg.bbuf == kBufWp && wp_leaf == kNoMap) wp_leaf = sg.src;
+          if (sg.tile_off % kChunkElems || sg.b_row + 16ull * sg.nchunks >= (1ull << 24))
+            return set_err(HMXG_EINVAL, "internal: CTree step out of range");
+          const std::uint32_t lim = sg.rows ? (sg.rows + 7) / 8 : 8u;
+          for (std::uint32_t ch = 0; ch < sg.nchunks; ++ch) {
+            const std::uint32_t nks = (ch + 1 == sg.nchunks && sg.last_ksteps) ? sg.last_ksteps : 4u;
+            for (std::uint32_t ks = 0; ks < nks; ++ks)
+              steps.push_back(CtStep{static_cast<std::uint32_t>((sg.tile_off / kChunkElems + ch) * 4 + ks),
+                                     (sg.b_row + ch * 16 + ks * 4) << 8 | std::uint32_t(sg.bbuf) << 4 | lim});
+          }
+          t_lo = std::min<std::uint64_t>(t_lo, sg.tile_off);
+          t_hi = std::max<std::uint64_t>(t_hi, sg.tile_off + std::uint64_t(sg.nchunks) * kChunkElems);
+        }
+        if (tk.id_off != kNoMap && tk.id_buf == kBufWp && wp_leaf == kNoMap) wp_leaf = tk.id_node0;
+        tk.seg_begin = kb;
+        tk.seg_end = static_cast<std::uint32_t>(steps.size());
+        tk.pad1 = wp_leaf;
+        const std::uint32_t lt = static_cast<std::uint32_t>(tasks.size());
+        tasks.push_back(tk);
+        for (std::uint32_t o = 0; o * 8 < tk.m; o += kCtG) units.push_back(lt << 5 | o);
+      }
+      lvl.push_back(static_cast<std::uint32_t>(units.size()));
+    }
+    if (steps.size() >= (1ull << 32) / kChunkElems) return set_err(HMXG_EINVAL, "internal: CTree program too large");
+    const std::size_t tb = (tasks.size() * sizeof(Task) + 15) / 16 * 16;
+    const std::size_t sb = (steps.size() * sizeof(CtStep) + 15) / 16 * 16;
+    std::vector<unsigned char> blob(tb + sb, 0);
+    std::memcpy(blob.data(), tasks.data(), tasks.size() * sizeof(Task));
+    if (!steps.empty()) std::memcpy(blob.data() + tb, steps.data(), steps.size() * sizeof(CtStep));
+    HMXG_TRY(dev_upload(&d.ct_blob, blob.data(), blob.size(), st));
+    HMXG_TRY(dev_upload(&d.ct_units, units.data(), units.size(), st));
+    HMXG_TRY(dev_upload(&d.ct_lvl, lvl.data(), lvl.size(), st));
+    d.ct_nlev = static_cast<std::uint32_t>(lvl.size() - 1);
+    d.ct_blob_bytes = static_cast<std::uint32_t>(blob.size());
+    d.ct_segs_off = static_cast<std::uint32_t>(tb);
+    d.ct_tile_base = t_lo == ~0ull ? 0 : t_lo;
+    d.ct_tile_lines = t_hi > d.ct_tile_base ? (t_hi - d.ct_tile_base + 15) / 16 : 0;
+  }
   HMXG_CUDA(cudaStreamSynchronize(st));
   e.nitems = static_cast<std::uint32_t>(items.size());
   e.q = q;
   e.stage = stage;
+  e.ct = ct;
   *out = &e;
   return HMXG_OK;
 }
@@ -489,6 +641,42 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
                    r[7]);
     }
   std::fclose(f);
+  // CTree clusters: per CTA start, tables copied, end of each level
+  {
+    const std::string cpath = std::string(path) + ".ctree";
+    FILE* fc = std::fopen(cpath.c_str(), "w");
+    if (fc) {
+      std::fprintf(fc, "cta,oct,rank,t_start,t_tables,levels\n");
+      for (std::size_t b = 0; b < g_trace_words / (kTraceSeq * kTraceWords); ++b) {
+        const unsigned long long* r = &h[(b * kTraceSeq + kTraceSeq - 3) * kTraceWords];
+        if ((r[0] >> 48) != 0xc7eeull) continue;
+        std::fprintf(fc, "%zu,%llu,%llu,%llu,%llu,", b, (r[0] >> 8) & 0xffffffull, r[0] & 0xffull, r[1], r[2]);
+        for (int l = 0; l < 13 && r[3 + l]; ++l) std::fprintf(fc, "%s%llu", l ? ";" : "", r[3 + l]);
+        std::fprintf(fc, "\n");
+      }
+      std::fclose(fc);
+    }
+  }
+  {  // CTree units: per warp its first unit of level 0 [begin, waited, first block, end, unit|chunks]
+    const std::string upath = std::string(path) + ".ctunit";
+    FILE* fu = std::fopen(upath.c_str(), "w");
+    if (fu) {
+      std::fprintf(fu, "cta,warp,t_begin,t_waited,t_first,t_end,unit,chunks,blocks\n");
+      for (std::size_t b = 0; b < g_trace_words / (kTraceSeq * kTraceWords); ++b) {
+        const unsigned long long* r0 = &h[(b * kTraceSeq + kTraceSeq - 3) * kTraceWords];
+        if ((r0[0] >> 48) != 0xc7eeull) continue;
+        for (int w = 0; w < 5; ++w) {
+          const unsigned long long* r = &h[(b * kTraceSeq + kTraceSeq - 8 - 15) * kTraceWords + w * 24];
+          if (!r[0]) continue;
+          std::fprintf(fu, "%zu,%d,%llu,%llu,%llu,%llu,%llu,%llu,", b, w, r[0], r[1], r[2], r[3], r[4] >> 32,
+                       r[4] & 0xffffffffull);
+          for (int k = 0; k < 12 && r[5 + k]; ++k) std::fprintf(fu, "%s%llu", k ? ";" : "", r[5 + k] - r[1]);
+          std::fprintf(fu, "\n");
+        }
+      }
+      std::fclose(fu);
+    }
+  }
   // the fused permute jobs: per CTA start, stores done, signal released
   const std::string ppath = std::string(path) + ".perm";
   FILE* fp = std::fopen(ppath.c_str(), "w");
@@ -571,8 +759,9 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   p.q = qq;
   if (!levels) {
     const DevState::DagItems* di = nullptr;
+    const bool ct = ctree_csize(plan, q, d.gemm_grid) != 0;
     for (const auto& e : d.dag)
-      if (e.items && e.q == q && e.stage == 0) di = &e;
+      if (e.items && e.q == q && e.stage == 0 && e.ct == ct) di = &e;
     if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
     const std::uint32_t cst = counter_stride(plan, q, d.gemm_grid);
     const std::size_t words = dag_done_words(plan, q, cst);
@@ -614,9 +803,50 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       p.y_final = y;
       p.ldy = ldy;
       p.pmap = d.pmap;
-      const unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, (n + 31) / 32 * dp.ncb));
+      unsigned fgrid = std::max<unsigned>(grid, std::min<unsigned>(d.gemm_grid, (n + 31) / 32 * dp.ncb));
+      const std::uint32_t csize = ctree_csize(plan, q, d.gemm_grid);
+      if (csize) {
+        if (!d.ct_units) return set_err(HMXG_ECUDA, "internal: CTree program not prepared");
+        dp.ct_noct = static_cast<std::uint32_t>((q + 7) / 8);
+        dp.ct_csize = csize;
+        dp.ct_nlev = d.ct_nlev;
+        dp.ct_units = d.ct_units;
+        dp.ct_lvl = d.ct_lvl;
+        dp.ct_blob = d.ct_blob;
+        dp.ct_blob_bytes = d.ct_blob_bytes;
+        dp.ct_segs_off = d.ct_segs_off;
+        dp.ct_tile_base = d.ct_tile_base;
+        p.y_final = nullptr;  // the final rows go to Yp; the clusters write Y
+        dp.y = y;
+        dp.ldy = ldy;
+        dp.ct_tile_lines = d.ct_tile_lines;
+        // every CTA in clusters of csize; the CTree clusters come on top of the item CTAs, and
+        // the grid stays within what is resident at once
+        HMXG_TRY(ct_resident(d, csize));
+        fgrid = std::min<unsigned>(fgrid + dp.ct_noct * csize, d.ct_occ_ctas);
+        fgrid -= fgrid % csize;
+        if (std::getenv("HMXG_DEBUG_LAUNCH"))
+          std::fprintf(stderr, "[hmxg] CTree launch: grid %u, clusters of %u, %u octet clusters, %u levels, resident %u\n",
+                       fgrid, csize, dp.ct_noct, dp.ct_nlev, d.ct_occ_ctas);
+      }
       HMXG_TRY(mark());
-      eval_dag<true><<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+      if (csize) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(fgrid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        HMXG_CUDA(cudaLaunchKernelEx(&cfg, eval_dag<true>, tm_wp, tm_t, tm_s, p, dp));
+      } else {
+        eval_dag<true><<<fgrid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, dp);
+      }
       ++*launches;
       HMXG_TRY(mark());
       HMXG_CUDA(cudaGetLastError());
@@ -1335,6 +1565,82 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
 }
 
 
+namespace hmxg {
+namespace {
+// hmxg_dag_check in CTree mode: the items are the near tiles, each once per column block and
+// part; the CTree levels hold every other task of the split variant exactly once, and every
+// T / S row block a level reads (B operand or identity rows) is complete at an earlier level;
+// the accumulating leaf rows read near tiles, which the items write completely.
+int ct_check(const Plan& plan, const std::vector<std::uint64_t>& items, std::uint32_t q, std::uint32_t S) {
+  const std::uint32_t ncb = (q + kBN - 1) / kBN;
+  const std::size_t nn = plan.num_nodes, nt = plan.tasks.size();
+  std::vector<std::uint8_t> is_near(nt, 0), in_ct(nt, 0);
+  for (const Phase& ph : plan.split_phases)
+    if (ph.kind == kPhaseNear)
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) is_near[t] = 1;
+  std::vector<std::uint8_t> seen(nt * std::size_t(ncb) * S, 0);
+  for (std::uint64_t it : items) {
+    const std::uint32_t t = static_cast<std::uint32_t>(it), cb = item_cb(it), sub = item_sub(it);
+    if (t >= nt || cb >= ncb || sub >= S || !is_near[t] || seen[(std::size_t(t) * ncb + cb) * S + sub]++)
+      return set_err(HMXG_EINVAL, "dag: CTree item list is not the near tiles x column blocks x parts");
+  }
+  if (items.size() != [&] {
+        std::size_t c = 0;
+        for (std::size_t t = 0; t < nt; ++t) c += is_near[t];
+        return c * ncb * S;
+      }())
+    return set_err(HMXG_EINVAL, "dag: a near tile is missing");
+  const std::vector<const Phase*> lv = ct_levels(plan);
+  std::vector<std::uint32_t> wr(3 * nn, 0), done(3 * nn, 0);
+  for (const Phase* ph : lv)
+    for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {
+      if (in_ct[t]++ || is_near[t]) return set_err(HMXG_EINVAL, "dag: a CTree task appears twice");
+      const Task& tk = plan.tasks[t];
+      if (tk.cbuf == kBufT) ++wr[tk.node];
+      if (tk.cbuf == kBufS) ++wr[nn + tk.node];
+    }
+  for (std::size_t t = 0; t < nt; ++t) {
+    if (is_near[t]) ++wr[2 * nn + plan.tasks[t].node];
+    if (!is_near[t] && !in_ct[t]) {  // a task of the combined leaf variant only
+      bool combined = false;
+      for (const Phase& ph : plan.phases)
+        if (ph.kind == kPhaseLeaf && t >= ph.task_begin && t < ph.task_end) combined = true;
+      if (!combined) return set_err(HMXG_EINVAL, "dag: a task is neither a near tile nor in the CTree");
+    }
+  }
+  for (std::size_t i = 0; i < nn; ++i) {
+    if (wr[i] && wr[i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: T writers != node tiles");
+    if (wr[nn + i] && wr[nn + i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: S writers != node tiles");
+    if (wr[2 * nn + i] != plan.yp_tiles[i]) return set_err(HMXG_EINVAL, "dag: Yp writers != near tiles");
+  }
+  auto ready = [&](std::size_t r) { return done[r] >= wr[r]; };
+  for (const Phase* ph : lv) {
+    for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {
+      const Task& tk = plan.tasks[t];
+      for (std::uint32_t sgi = tk.seg_begin; sgi < tk.seg_end; ++sgi) {
+        const SegDev& sg = plan.segs[sgi];
+        if ((sg.bbuf == kBufT || sg.bbuf == kBufS) && !(wr[(sg.bbuf == kBufT ? 0 : nn) + sg.src] &&
+                                                        ready((sg.bbuf == kBufT ? 0 : nn) + sg.src)))
+          return set_err(HMXG_EINVAL, "dag: a CTree level reads T / S rows of a later level");
+      }
+      if (tk.id_off != kNoMap && (tk.id_buf == kBufT || tk.id_buf == kBufS))
+        for (std::uint32_t nd : {tk.id_node0, tk.id_node1})
+          if (nd != kNoMap && !ready((tk.id_buf == kBufT ? 0 : nn) + nd))
+            return set_err(HMXG_EINVAL, "dag: a CTree level copies identity rows of a later level");
+      if (tk.flags & kTaskAccumulate && !wr[2 * nn + tk.node])
+        return set_err(HMXG_EINVAL, "dag: a CTree leaf task has no near tiles");
+    }
+    for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {  // the level's rows, after its reads
+      const Task& tk = plan.tasks[t];
+      if (tk.cbuf == kBufT) ++done[tk.node];
+      if (tk.cbuf == kBufS) ++done[nn + tk.node];
+    }
+  }
+  return HMXG_OK;
+}
+}  // namespace
+}  // namespace hmxg
+
 int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* nitems) {
   if (!cds || q == 0 || grid == 0) return set_err(HMXG_EINVAL, "hmxg_dag_check: null view, q = 0 or grid = 0");
   Plan plan;
@@ -1345,6 +1651,7 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   if (nitems) *nitems = items.size();
   const bool split = split_leaf(plan, q, grid);
   const std::uint32_t S = colsplit(plan, q, grid);  // parts per tile: every tile appears S times
+  if (ctree_csize(plan, q, grid)) return ct_check(plan, items, static_cast<std::uint32_t>(q), S);
   // (1) every task of the variant that runs, once per column block
   std::vector<std::uint32_t> want(plan.tasks.size(), 0), seen(plan.tasks.size() * std::size_t(ncb), 0);
   for (const Phase& ph : plan.phases)

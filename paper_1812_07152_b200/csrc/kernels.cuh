@@ -371,7 +371,7 @@ struct RingSlot {
 };
 static_assert(sizeof(RingSlot) == 192, "RingSlot layout");
 constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * sizeof(RingSlot) +
-                           3 * kSigRing * 8 + 8 + 1024;
+                           3 * kSigRing * 8 + 16 + 1024;
 
 struct CtaSmem {
   unsigned char* stage;    // kStages * kStageBytes, 1024-byte aligned
@@ -384,6 +384,7 @@ struct CtaSmem {
   std::uint64_t* sempty;   // [kSigRing] the producer took the record
   std::uint64_t* saddr;    // [kSigRing]
   std::uint64_t* pbar;     // eval_dag fused mode: the CTA's permute jobs are done (stages free)
+  std::uint64_t* ctbar;    // eval_dag CTree mode: the program tables have landed
 };
 
 __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
@@ -399,6 +400,7 @@ __device__ __forceinline__ CtaSmem carve_smem(unsigned char* smem_raw) {
   c.sempty = c.sfull + kSigRing;
   c.saddr = c.sempty + kSigRing;
   c.pbar = c.saddr + kSigRing;
+  c.ctbar = c.pbar + 1;
   return c;
 }
 
@@ -417,6 +419,7 @@ __device__ __forceinline__ void init_barriers(const CtaSmem& c) {
       mbar_init(&c.sempty[s], 1);
     }
     mbar_init(c.pbar, 1);
+    mbar_init(c.ctbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -784,6 +787,19 @@ struct DagParams {
   // as they are (the split fallback's stage 0, whose T counters stage 1 reads).
   std::uint32_t reset_words;
   std::uint32_t* exit_ctr;
+  // CTree mode (small problems, fused): every task but the near field runs inside clusters of
+  // ct_csize CTAs, one cluster per 8-column octet of W (the first ct_noct * ct_csize CTAs),
+  // level by level with cluster barriers in between; the item list holds the near tiles only.
+  // ct_blob: the CTree's tasks (k-step ranges) then, at byte ct_segs_off, their k steps
+  // (CtStep); copied to shared memory. ct_units: (local task << 5 | log2 G << 3 | first row octet) work
+  // units of G octets, level l = [ct_lvl[l], ct_lvl[l + 1]); ct_tile_base / ct_tile_lines: the
+  // A chunks they read (128-byte lines from the tiles' element offset ct_tile_base), prefetched
+  // into L2. The final rows go to Yp; each cluster then writes its octet of Y through ipmap.
+  std::uint32_t ct_noct, ct_csize, ct_nlev, ct_blob_bytes, ct_segs_off;
+  const void* ct_blob;
+  const std::uint32_t* ct_units;
+  const std::uint32_t* ct_lvl;
+  std::uint64_t ct_tile_base, ct_tile_lines;
 #ifdef HMXG_TRACE
   // diagnostic builds (tools/dag_trace.py): per claimed item, kTraceWords globaltimer stamps
   unsigned long long* trace;
@@ -882,6 +898,305 @@ __device__ __forceinline__ void dag_exit(const DagParams& d) {
   if (threadIdx.x == 0) *d.exit_ctr = 0u;
 }
 
+// ---------------------------------------------------------------- CTree (small problems)
+// MatRox's coarsened sub-tree execution (executor.cpp:139-190, structure.cpp:147-186: one
+// worker runs a whole disjoint sub-tree with no barrier between its internal levels) on the
+// B200: the columns of W are independent, so the whole tree of one 8-column octet is the
+// disjoint unit. A cluster of CTAs runs its levels -- upward, far+downward and the leaf rows
+// -- separated by cluster barriers (shared-memory-speed) instead of the DAG's gpu-scope
+// release / poll / L2 reload per level (~4 us each, the whole of cfg1's step). Only the
+// near field (the bulk of the flops, no tree dependency) stays in the DAG's item list, and
+// the leaf rows wait for its tiles. Operands are read straight from global memory (A from
+// the pre-tiled chunks, B rows of T / S from L2, Wp rows as W[pmap[row], col]) and the
+// final rows are stored into Y through pmap. Every 8 x 8 output fragment runs the DAG's
+// exact DMMA sequence (accumulator start, segments, chunks, k steps, identity rows last for
+// leaf rows), so the results are bit-identical to the DAG and the level launches.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// The CTree program in shared memory (one bulk copy at the start): its tasks and, per task,
+// the flat list of its k steps in the DAG's order (segment, chunk, k step), so that no operand
+// address waits on a global load and the loop body stays a few dozen instructions (the
+// instruction cache, not the math, bounded the first version).
+// CtTask: Task with seg_begin / seg_end = the task's k-step range, pad1 = the leaf whose Wp
+// rows it reads (kNoMap: none). CtStep: A = chunk * 4 + k step (the lanes add their k and
+// row), B = row << 8 | buffer << 4 | live octet limit (ceil(SegDev::rows / 8), 8 = all).
+struct CtStep {
+  std::uint32_t a, b;
+};
+struct CtSmem {
+  const Task* tasks;
+  const CtStep* steps;
+};
+// An element of a B operand or identity row: buffer b (Wp, T, S, Yp), padded row, logical
+// column. Written during this launch by other CTAs: read at L2 (after the acquire).
+__device__ __forceinline__ double ct_load(const GemmParams& p, unsigned b, std::uint32_t row, std::uint32_t col) {
+  return __ldcg(pick_buf(p, b) + static_cast<std::uint64_t>(row) * pick_ld(p, b) + phys_col(col));
+}
+// Counter of (node, column block) in a completion region of stride cst.
+template <class D>
+__device__ __forceinline__ std::uint64_t at_node(const D& d, std::uint32_t node, std::uint32_t cb, std::uint64_t cst) {
+  return (static_cast<std::uint64_t>(node) * d.ncb + cb) * cst;
+}
+// Lane 0 waits for a counter, then every lane acquires it.
+__device__ __noinline__ void ct_wait(const std::uint32_t* ctr, std::uint32_t target) {
+  if ((threadIdx.x & 31) == 0) spin_until(ctr, target);
+  __syncwarp();
+  (void)ld_acquire(ctr);
+}
+
+#ifndef HMXG_CT_G
+#define HMXG_CT_G 2
+#endif
+constexpr int kCtG = HMXG_CT_G;  // row octets per CTree unit
+#ifndef HMXG_CT_ALD
+#define HMXG_CT_ALD __ldg
+#endif
+// One work unit -- G consecutive 8-row octets of a task x the column octet's 8 columns -- on
+// one warp: G independent DMMA chains; two register blocks of KB k steps, the next block's
+// loads in flight while the current one multiplies.
+template <int G>
+__device__ __forceinline__ void ct_unit(const GemmParams& p, const DagParams& d, const CtSmem& cs,
+                                       std::uint32_t unit, std::uint32_t cb, std::uint32_t col0,
+                                       std::uint32_t ncols, std::uint32_t* done_y, std::uint32_t* done_w,
+                                       std::uint64_t cst, std::uint32_t wmul, unsigned long long* ust = nullptr) {
+  constexpr int KB = G == 1 ? 6 : (G == 2 ? 3 : 2);  // k steps per register block
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  const Task task = cs.tasks[unit >> 5];
+  const std::uint32_t oct0 = unit & 7u;
+  const int noct = min(G, static_cast<int>((task.m + 7) / 8) - static_cast<int>(oct0));
+  const bool bcol_ok = static_cast<std::uint32_t>(fr) < ncols;  // the lane's B column
+  const std::uint32_t bcol = col0 + fr;
+  const std::uint32_t cc = 2 * fk;  // the lane's C columns cc, cc + 1 within the octet
+#ifdef HMXG_TRACE
+  if (ust && lane == 0) ust[0] = gtimer();
+#endif
+  if (task.pad1 != kNoMap) ct_wait(done_w + at_node(d, task.pad1, cb, cst), d.wp_target[task.pad1]);
+#ifdef HMXG_TRACE
+  if (ust && lane == 0) ust[1] = gtimer();
+#endif
+  double acc[G][2];
+#pragma unroll
+  for (int o = 0; o < G; ++o) acc[o][0] = acc[o][1] = 0.0;
+  const bool has_id = task.id_off != kNoMap;
+  const bool id_last = (task.flags & kTaskIdLast) != 0;
+  std::uint32_t src[G];
+#pragma unroll
+  for (int o = 0; o < G; ++o) {
+    const std::uint32_t row = (oct0 + o) * 8 + fr;
+    src[o] = has_id && o < noct && row < task.m ? __ldg(p.idmap + task.id_off + row) : kNoMap;
+  }
+  // rows (own rows, identity rows) into the accumulators: acc[o] = (add ? acc[o] : 0) + row
+#define HMXG_CT_ROWS_IN(B, SRC_OF, ADD)                                                 \
+  _Pragma("unroll") for (int o = 0; o < G; ++o) {                                        \
+    if (o < noct) {                                                                      \
+      const std::uint32_t s_ = (SRC_OF);                                                 \
+      double v0 = 0.0, v1 = 0.0;                                                         \
+      if (s_ != kNoMap) {                                                                \
+        if (cc < ncols) v0 = ct_load(p, (B), s_, col0 + cc);                             \
+        if (cc + 1 < ncols) v1 = ct_load(p, (B), s_, col0 + cc + 1);                     \
+      }                                                                                  \
+      acc[o][0] = (ADD) ? acc[o][0] + v0 : v0;                                           \
+      acc[o][1] = (ADD) ? acc[o][1] + v1 : v1;                                           \
+    }                                                                                    \
+  }
+  // the k steps of the task, in the DAG's order, skipping those with no live octet here
+  const std::uint32_t k0 = task.seg_begin, k1 = task.seg_end;
+  const int lane_a = fk * kBM;  // + (row ^ (fk << 2)) per octet
+  double a0[KB][G], b0[KB], a1[KB][G], b1[KB];
+  std::uint32_t n0 = 0, n1 = 0;  // live octets of k step j at bits 3j
+  std::uint32_t kn = k0;
+  auto load_blk = [&](double (&a)[KB][G], double (&b)[KB], std::uint32_t& nl) {
+    int c = 0;
+    nl = 0;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      int live = 0;
+      CtStep st{};
+      while (kn < k1) {  // (dead steps: rows-limited segments below this unit's octets)
+        st = cs.steps[kn++];
+        live = min(noct, static_cast<int>(st.b & 15u) - static_cast<int>(oct0));
+        if (live > 0) break;
+      }
+      if (live > 0) {
+        const double* ach = p.tiles + static_cast<std::uint64_t>(st.a >> 2) * kChunkElems + (st.a & 3u) * 4 * kBM + lane_a;
+#pragma unroll
+        for (int o = 0; o < G; ++o)
+          if (o < live) a[j][o] = HMXG_CT_ALD(ach + ((((oct0 + o) * 8 + fr)) ^ (fk << 2)));
+        b[j] = bcol_ok ? ct_load(p, (st.b >> 4) & 15u, (st.b >> 8) + fk, bcol) : 0.0;
+        nl |= static_cast<std::uint32_t>(live) << (3 * j);
+        c = j + 1;
+      }
+    }
+    return c;
+  };
+  auto mul_blk = [&](const double (&a)[KB][G], const double (&b)[KB], std::uint32_t nl, int c) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < c)
+#pragma unroll
+        for (int o = 0; o < G; ++o)
+          if (o < static_cast<int>((nl >> (3 * j)) & 7u)) dmma884(acc[o], a[j][o], b[j]);
+  };
+  // the first two blocks' operands go out before the accumulator's start rows are waited
+  // for (a leaf task's near tiles may still be in flight)
+  int c0 = load_blk(a0, b0, n0);
+  int c1 = c0 ? load_blk(a1, b1, n1) : 0;
+  if (task.flags & kTaskAccumulate) {  // the near tiles of this leaf (DAG items) are stored
+    ct_wait(done_y + at_node(d, task.node, cb, cst), d.yp_tiles[task.node] * wmul);
+    HMXG_CT_ROWS_IN(task.cbuf, (oct0 + o) * 8 + fr < task.m ? task.c_row + (oct0 + o) * 8 + fr : kNoMap, false)
+  }
+  if (has_id && !id_last) {
+    if (task.flags & kTaskAccumulate) {
+      HMXG_CT_ROWS_IN(task.id_buf, src[o], true)
+    } else {
+      HMXG_CT_ROWS_IN(task.id_buf, src[o], false)
+    }
+  }
+#ifdef HMXG_TRACE
+  int blk_ = 0;
+  // per block: DMMAs done (the accumulator read forces completion), up to 12 blocks
+#define HMXG_CT_BSTAMP()                                                                          \
+  if (ust && lane == 0 && blk_ < 12) {                                                           \
+    double z_ = acc[0][0];                                                                       \
+    asm volatile("" : "+d"(z_));                                                                 \
+    ust[5 + blk_] = gtimer() + (z_ == 12345.678 ? 1ull : 0ull);                                  \
+  }                                                                                              \
+  ++blk_;
+#else
+#define HMXG_CT_BSTAMP()
+#endif
+  while (c0) {
+    mul_blk(a0, b0, n0, c0);
+    HMXG_CT_BSTAMP()
+    if (!c1) break;
+    c0 = load_blk(a0, b0, n0);
+    mul_blk(a1, b1, n1, c1);
+    HMXG_CT_BSTAMP()
+    if (!c0) break;
+    c1 = load_blk(a1, b1, n1);
+  }
+#undef HMXG_CT_BSTAMP
+  if (has_id && id_last) {
+    HMXG_CT_ROWS_IN(task.id_buf, src[o], true)
+  }
+#undef HMXG_CT_ROWS_IN
+  double* const cbase = pick_buf(p, task.cbuf);
+  const std::uint64_t ldc = pick_ld(p, task.cbuf);
+#pragma unroll
+  for (int o = 0; o < G; ++o) {
+    const std::uint32_t row = (oct0 + o) * 8 + fr;
+    if (o >= noct || row >= task.m) continue;
+    double* crow = cbase + static_cast<std::uint64_t>(task.c_row + row) * ldc + phys_col(col0 + cc);
+    if (cc + 1 < ncols)
+      __stcg(reinterpret_cast<double2*>(crow), make_double2(acc[o][0], acc[o][1]));
+    else if (cc < ncols)
+      __stcg(crow, acc[o][0]);
+  }
+#ifdef HMXG_TRACE
+  if (ust && lane == 0) {
+    ust[3] = gtimer();
+    ust[4] = (static_cast<unsigned long long>(unit) << 32) | (k1 - k0);
+  }
+  if (ust && lane == 0) ust[2] = ust[5];
+#endif
+}
+
+// A CTree cluster: octet `oct` of the columns, this CTA's rank in the cluster. Every thread of
+// every CTA of the cluster runs the same number of cluster barriers. `c.stage` holds the
+// program tables (the CTA joins the item loop afterwards, when the stages are free again).
+__device__ __forceinline__ void ct_run(const GemmParams& p, const DagParams& d, const CtaSmem& c,
+                                      std::uint32_t oct, std::uint32_t rank, std::uint32_t* done_y,
+                                      std::uint32_t* done_w, std::uint64_t cst, std::uint32_t wmul) {
+  const std::uint32_t cb = oct / (kBN / 8), col0 = oct * 8;
+  const std::uint32_t ncols = min(8u, p.q - col0);
+#ifdef HMXG_TRACE
+  const unsigned long long t_start = gtimer();
+#endif
+  if (threadIdx.x == 0) {  // the tables: bulk copies of <= 32 KB (sizes are multiples of 16)
+    mbar_expect_tx(c.ctbar, d.ct_blob_bytes);
+    for (std::uint32_t off = 0; off < d.ct_blob_bytes; off += 32768u)
+      bulk_g2s(c.stage + off, reinterpret_cast<const unsigned char*>(d.ct_blob) + off,
+               min(32768u, d.ct_blob_bytes - off), c.ctbar);
+  }
+  {  // the A chunks into L2 meanwhile (after an L2 flush they would come from DRAM at the level
+     // that first reads them): this cluster's share of the program's range
+    const std::uint32_t tid = rank * kThreads + threadIdx.x, nt = d.ct_csize * kThreads;
+    for (std::uint64_t l = tid + static_cast<std::uint64_t>(oct) * nt; l < d.ct_tile_lines; l += nt * d.ct_noct)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.tiles + d.ct_tile_base + l * 16));
+  }
+  mbar_wait(c.ctbar, 0);
+  const CtSmem cs{reinterpret_cast<const Task*>(c.stage), reinterpret_cast<const CtStep*>(c.stage + d.ct_segs_off)};
+#ifdef HMXG_TRACE
+  // trace builds: [marker | oct << 8 | rank, start, tables copied, level 0 end, ...] in the
+  // CTA's last-but-one two trace slots (16 words)
+  unsigned long long* ctr_ = d.trace + (static_cast<std::uint64_t>(blockIdx.x) * kTraceSeq + kTraceSeq - 3) * kTraceWords;
+  if (threadIdx.x == 0) {
+    ctr_[0] = 0xc7ee000000000000ull | (static_cast<unsigned long long>(oct) << 8) | rank;
+    ctr_[1] = t_start;
+    ctr_[2] = gtimer();
+  }
+#endif
+  const std::uint32_t warps = kThreads / 32;
+  const std::uint32_t gw = rank * warps + (threadIdx.x >> 5), nw = d.ct_csize * warps;
+  for (std::uint32_t l = 0; l < d.ct_nlev; ++l) {
+    const std::uint32_t u0 = __ldg(d.ct_lvl + l), u1 = __ldg(d.ct_lvl + l + 1);
+    for (std::uint32_t u = u0 + gw; u < u1; u += nw) {
+      const std::uint32_t unit = __ldg(d.ct_units + u);
+      // one instantiation (kCtG octets per unit): two or more inlined bodies make ptxas spill
+      // the whole kernel at its 128-register bound
+#ifdef HMXG_TRACE
+      // per warp, its first unit of level 0 (5 words) in the trace slots below the CTree record
+      unsigned long long* ust = nullptr;
+      if (u < u0 + nw && l == 0)
+        ust = d.trace + (static_cast<std::uint64_t>(blockIdx.x) * kTraceSeq + kTraceSeq - 8 - 3 * 5) * kTraceWords +
+              (threadIdx.x >> 5) * 24;
+      ct_unit<kCtG>(p, d, cs, unit, cb, col0, ncols, done_y, done_w, cst, wmul, ust);
+#else
+      ct_unit<kCtG>(p, d, cs, unit, cb, col0, ncols, done_y, done_w, cst, wmul);
+#endif
+    }
+#ifdef HMXG_TRACE
+    if (l < 12) {
+      __syncthreads();
+      if (threadIdx.x == 0) ctr_[3 + l] = gtimer();
+    }
+#endif
+    cluster_sync_all();  // this level's rows before the next level (or the scatter) reads them
+  }
+  // Y[:, octet] = Yp rows through ipmap, this CTA's share of the points: every near tile is
+  // stored (the leaves without a basis have no CTree task that waited for theirs)
+  for (std::uint32_t i = threadIdx.x; i < d.nodes; i += kThreads)
+    if (d.yp_tiles[i]) {
+      const std::uint32_t* ctr = done_y + at_node(d, i, cb, cst);
+      spin_until(ctr, d.yp_tiles[i] * wmul);
+    }
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  __syncthreads();
+  const double* yp = p.buf[kBufYp] + phys_col(col0);
+  const std::uint64_t ldyp = p.ld[kBufYp];
+  const std::uint32_t per = (d.n + d.ct_csize - 1) / d.ct_csize;
+  const std::uint32_t r1 = min(d.n, (rank + 1) * per);
+  for (std::uint32_t r = rank * per + threadIdx.x; r < r1; r += kThreads) {
+    const double* src = yp + static_cast<std::uint64_t>(__ldg(d.ipmap + r)) * ldyp;
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const double2 x = __ldcg(reinterpret_cast<const double2*>(src + u));
+      v[u] = x.x;
+      v[u + 1] = x.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (static_cast<std::uint32_t>(u) < ncols) d.y[r + static_cast<std::uint64_t>(col0 + u) * d.ldy] = v[u];
+  }
+#ifdef HMXG_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) ctr_[15] = gtimer();
+#endif
+  __syncthreads();  // the stage area is the producer's again
+}
+
 // kNarrow: the instantiation for narrow DAGs (column-split items, padded counters, fused
 // permutations, self-reset); the wide one compiles those paths out (they cost the cfg5 DAG
 // 3.8% as runtime branches).
@@ -902,6 +1217,11 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   std::uint32_t* const done_w = done_y + region;
   auto at = [&](std::uint32_t node, std::uint32_t cb) { return (static_cast<std::uint64_t>(node) * d.ncb + cb) * cst; };
   const std::uint32_t wmul = kConsumerWarps * (kNarrow ? d.colsplit : 1);  // signals per complete row tile
+  // CTree mode: the first ct_ctas CTAs are the octet clusters; they run their trees first and
+  // then join the item loop (which by then only has the end item for them)
+  const std::uint32_t ct_ctas = kNarrow ? d.ct_noct * d.ct_csize : 0u;
+  const bool ct_cta = kNarrow && blockIdx.x < ct_ctas;
+  if (kNarrow && ct_cta) ct_run(p, d, c, blockIdx.x / d.ct_csize, blockIdx.x % d.ct_csize, done_y, done_w, cst, wmul);
 
   if (kNarrow && d.fused && warp < kConsumerWarps) {
     // Wp[ipmap[r]][phys(c)] = W[r + c ldw] in source order: a job is 32 consecutive points x
@@ -917,7 +1237,9 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     if (tid == 0) ptr_[1] = gtimer();
 #endif
     const std::uint32_t nblk = (d.n + 31) / 32;
-    for (std::uint32_t job = blockIdx.x; job < nblk * d.ncb; job += gridDim.x) {
+    // the CTree clusters read W directly: the other CTAs gather Wp for the near tiles
+    for (std::uint32_t job = ct_cta ? nblk * d.ncb : blockIdx.x - ct_ctas; job < nblk * d.ncb;
+         job += gridDim.x - ct_ctas) {
       const std::uint32_t r0 = (job / d.ncb) * 32, cb = job % d.ncb;
       const std::uint32_t ncols = min(static_cast<std::uint32_t>(kBN), p.q - cb * kBN);
       const std::uint32_t nr = min(32u, d.n - r0);
@@ -1092,7 +1414,8 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
     // phase accumulates onto the near phase's rows of the same leaf)
     release_item(c, seq);
     // final leaf rows have no reader inside the launch (the split variant's near rows do)
-    const bool publish = task.cbuf != kBufYp || (d.signal_yp && !(task.flags & kTaskFinal));
+    // (CTree mode: every near tile, the clusters read them all)
+    const bool publish = task.cbuf != kBufYp || (d.signal_yp && !(task.flags & kTaskFinal)) || (kNarrow && d.ct_noct);
     std::uint32_t* const ctr = (task.cbuf == kBufT ? done_t : (task.cbuf == kBufS ? done_s : done_y)) + at(task.node, cb);
     if (d.fwd_signals)
       post_signal(seq, publish ? reinterpret_cast<std::uint64_t>(ctr) : 0);

@@ -160,6 +160,8 @@ struct Plan {
   std::vector<std::uint32_t> maps;
   std::vector<std::uint32_t> idmap;
   double identity_flops_per_col = 0.0;  // multiply-adds by exact 0/1 rows the kernel skips
+  mutable double ct_dmma = -1.0;         // CTree work per 8-column octet in DMMAs (hmxg.cu, cached)
+  mutable std::uint64_t ct_smem = 0;     // its tables' shared-memory bytes
 };
 
 // Validates the view (structure.hpp invariants the evaluator relies on) and lowers it.

@@ -418,3 +418,41 @@ def test_fused_small_problem_launch_equals_three_launches(name, q, monkeypatch):
     assert np.array_equal(ev.evaluate(w), fused)  # counters left clean by either launch sequence
     assert oracle.rel_frob(fused, oracle.oracle_evaluate(inst.cds, w)) <= TOL
     ev.close()
+
+
+@pytest.mark.parametrize("name,q", [("cfg1-hss", 64), ("cfg1-hss", 37), ("tiny", 9), ("ragged", 100)])
+def test_ctree_mode_gives_the_dag_bits(name, q, monkeypatch):
+    """CTree mode (HMXG_CTREE=1, MatRox's coarsened sub-tree execution: every task but the near
+    field runs inside one CTA cluster per 8-column octet, levels separated by cluster barriers)
+    runs each 8 x 8 fragment's exact DMMA sequence of the DAG: the same bits as the DAG launch
+    and the level launches, through the host and the device paths, for 2, 4 and 8-CTA clusters."""
+    import torch
+
+    if name == "tiny":
+        inst = build_instance(InstanceSpec(n=129, d=3, leaf=16, max_rank=12, seed=3))
+    elif name == "ragged":
+        inst = build_instance(InstanceSpec(n=1500, d=5, leaf=40, max_rank=24, mode="budget", budget=0.1, seed=9,
+                                           kernel="exponential", h=1.5))
+    else:
+        inst = build_instance(config(name)[0])
+    n = inst.cds.n
+    ev = Evaluator(inst.cds)
+    w = _w(n, q, 23)
+    dag = ev.evaluate(w)
+    lev = ev.evaluate(w, levels=True)
+    assert np.array_equal(dag, lev)
+    monkeypatch.setenv("HMXG_CTREE", "1")
+    wd = torch.from_numpy(w.T.copy()).cuda()
+    yd = torch.empty_like(wd)
+    for cs in ("2", "4", "8"):
+        monkeypatch.setenv("HMXG_CT_CLUSTER", cs)
+        assert np.array_equal(ev.evaluate(w), dag), cs
+        yd.fill_(np.nan)
+        ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, stream=torch_stream(), graph=False, sync=True)
+        assert np.array_equal(yd.cpu().numpy().T, dag), cs
+    assert np.array_equal(ev.evaluate(w, levels=True), dag)
+    monkeypatch.delenv("HMXG_CTREE")
+    assert np.array_equal(ev.evaluate(w), dag)  # counters and item lists clean after the mode switch
+    assert oracle.rel_frob(dag, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    ev.close()
+    inst.close()

@@ -288,3 +288,23 @@ def test_cds_fingerprint_sees_every_edit():
     cds.perm[[0, 1]] = cds.perm[[1, 0]]
     other = build_instance(InstanceSpec(n=1500, d=3, leaf=40, max_rank=24, mode="budget", budget=0.1, h=0.4, seed=3))
     assert other.cds.fingerprint() != fp
+
+
+def test_dag_check_ctree_mode(monkeypatch):
+    """CTree mode (HMXG_CTREE=1): the item list is the near tiles only (x column blocks x
+    parts), and the CTree levels hold every other task of the split variant once, each level
+    reading only rows of earlier levels (hmxg_dag_check's CTree branch)."""
+    from paper_1812_07152_b200 import config
+
+    insts = [build_instance(config("cfg1-hss")[0]), _small(),
+             build_instance(InstanceSpec(n=1500, d=5, leaf=40, max_rank=24, mode="budget", budget=0.1, seed=9))]
+    for inst in insts:
+        v = inst.cds.view()
+        for q in (8, 37, 64, 100):
+            n_dag, n_ct = C.c_uint64(), C.c_uint64()
+            monkeypatch.delenv("HMXG_CTREE", raising=False)
+            assert N.hmxg().hmxg_dag_check(C.byref(v), q, 444, C.byref(n_dag)) == 0, N.last_error(N.hmxg(), "hmxg")
+            monkeypatch.setenv("HMXG_CTREE", "1")
+            assert N.hmxg().hmxg_dag_check(C.byref(v), q, 444, C.byref(n_ct)) == 0, N.last_error(N.hmxg(), "hmxg")
+            assert 0 < n_ct.value < n_dag.value  # the near tiles only
+        inst.close()

@@ -41,6 +41,8 @@ def summarize(path: str) -> None:
         for k in ("t_claim", "t_issued", "t_take", "t_kend", "t_done", "t_first", "t_deps", "chunks"):
             r[k] = int(r[k])
     t0 = min(r["t_claim"] for r in rows)
+    if os.path.exists(path + ".ctree"):
+        t0 = min([t0] + [int(r["t_start"]) for r in csv.DictReader(open(path + ".ctree"))])
     t1 = max(r["t_done"] for r in rows)
     print(f"{path}: {len(rows)} items, launch span {(t1 - t0) / 1e3:.1f} us")
     ph = defaultdict(list)
@@ -64,6 +66,27 @@ def summarize(path: str) -> None:
         dp = sum(dp) / len(dp) / 1e3 if dp else float("nan")
         print(f"{KIND.get(k[0], k[0]):>6} L{k[1]:<2} {n:>6} {ch:6.1f} {first:8.2f} {last:8.2f} {ct:10.2f} {tk:10.2f} "
               f"{kd:10.2f} {t1:9.2f} {dp:10.2f}")
+    if os.path.exists(path + ".ctree"):  # CTree clusters (small problems): level ends
+        cr = list(csv.DictReader(open(path + ".ctree")))
+        if cr:
+            lv = [[(int(x) - t0) / 1e3 for x in r["levels"].split(";") if x] for r in cr]
+            st = [(int(r["t_start"]) - t0) / 1e3 for r in cr]
+            tb = [(int(r["t_tables"]) - t0) / 1e3 for r in cr]
+            print(f"  CTree: {len(cr)} CTAs, start {min(st):.2f}..{max(st):.2f}, tables {min(tb):.2f}..{max(tb):.2f} us")
+            for l in range(max(len(v) for v in lv)):
+                e = sorted(v[l] for v in lv if len(v) > l)
+                print(f"    level {l:2d} end: min {e[0]:8.2f} median {e[len(e) // 2]:8.2f} max {e[-1]:8.2f} us")
+    if os.path.exists(path + ".ctunit"):  # CTree: each warp's first unit of level 0
+        ur = list(csv.DictReader(open(path + ".ctunit")))
+        if ur:
+            def med(f):
+                v = sorted(f(r) for r in ur)
+                return v[len(v) // 2], v[-1]
+            for name, f in (("begin", lambda r: int(r["t_begin"]) - t0), ("wait", lambda r: int(r["t_waited"]) - int(r["t_begin"])),
+                            ("first block", lambda r: int(r["t_first"]) - int(r["t_waited"])),
+                            ("rest", lambda r: int(r["t_end"]) - int(r["t_first"])), ("chunks", lambda r: int(r["chunks"]) * 1000)):
+                m, x = med(f)
+                print(f"    level-0 unit {name:>11}: median {m / 1e3:8.2f} max {x / 1e3:8.2f}")
     if os.path.exists(path + ".perm"):  # fused permute jobs (small problems)
         pr = list(csv.DictReader(open(path + ".perm")))
         if pr:
