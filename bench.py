@@ -465,6 +465,58 @@ def measure(args, name, env, steps, warmup, e2e_steps, dropin_steps):
     return out
 
 
+def measure_near_otf(args, name, env, steps, warmup):
+    """The near field generated on the fly (HMXG_UPLOAD_NEAR_ON_THE_FLY): the config built
+    without D on the host, uploaded with points + kernel, every evaluation generating its near
+    blocks wave by wave into a bounded scratch. Device-resident, this rank's column shard."""
+    import torch
+
+    from paper_1812_07152_b200 import Evaluator, build_instance, config
+    from paper_1812_07152_b200.accuracy import Kernel
+    from paper_1812_07152_b200.distributed import column_shard
+
+    rank, world, local, dev, barrier, allmax = (env[k] for k in ("rank", "world", "local", "dev", "barrier", "allmax"))
+    spec, q_total = config(name)
+    spec.skip_near = True
+    if world > 1:
+        spec.threads = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+    inst = build_instance(spec)
+    cds = inst.cds
+    c0, c1 = column_shard(q_total, world, rank)
+    q = c1 - c0
+    ev = Evaluator(cds, devices=(local,), points=inst.points(), kernel=Kernel(spec.kernel, spec.h), near_on_the_fly=True)
+    w = torch.randn((q, cds.n), dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(7))
+    y = torch.empty_like(w)
+    stream = torch.cuda.Stream(device=dev)
+    for _ in range(warmup):
+        ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=stream.cuda_stream, time_phases=True)
+    torch.cuda.synchronize()
+    barrier()
+    ms = []
+    gen_ms = leaf_ms = 0.0
+    with ClockSampler(local) as clocks:
+        for _ in range(steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ev.evaluate_device(w.data_ptr(), y.data_ptr(), q, stream=stream.cuda_stream, time_phases=True)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            ph = ev.phases()
+            gen_ms += sum(p["ms"] for p in ph if p["kind"] == "near-gen")
+            leaf_ms += sum(p["ms"] for p in ph if p["kind"] == "near+leaf")
+    ms_step = allmax(sum(ms)) / steps
+    waves = sum(1 for p in ev.phases() if p["kind"] == "near-gen")
+    out = {"workload": DESCR.get(name, name) + "; near blocks generated on the fly (never resident)",
+           "value": cds.flops(q_total) / (ms_step * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_step,
+           "q_per_gpu": q, "device_gb": ev.info().device_bytes / 1e9, "near_gb_not_resident": 8 * float(cds.dptr[-1]) / 1e9,
+           "waves": waves, "near_gen_ms_per_step": gen_ms / steps, "leaf_waves_ms_per_step": leaf_ms / steps,
+           "clocks": clocks.summary()}
+    ev.close()
+    inst.close()
+    return out
+
+
 def ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -519,6 +571,9 @@ def ours(args) -> None:
                 "gpu_launches": x["launches"], "clocks": x["clk"], "phases_ms": x["phases_ms"], "cds": x["cds_info"],
                 "cds_gb": x["cds_gb"]}
 
+    if args.extra and args.config == "cfg5-hss" and args.near_otf:
+        extra["cfg5_h2b_near_on_the_fly"] = measure_near_otf(args, "cfg5-h2b", env, max(3, args.steps // 2), args.warmup)
+
     clk_all = [m["clk"]]
     if world > 1:
         clk_all = [None] * world
@@ -564,6 +619,7 @@ def main():
     ap.add_argument("--dropin-steps", type=int, default=2)
     ap.add_argument("--extra", default="cfg5-h2b", help="comma list of configs measured into `extra` (cfg5-hss runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--near-otf", type=int, default=1, help="measure cfg5-h2b with the near field on the fly (extra)")
     ap.add_argument("--cpu-step-s", type=float, default=8.0, help="target seconds of the cpu_baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=3.0, help="target seconds per reference-arm step")
     ap.add_argument("--ref-threads", type=int, default=1)

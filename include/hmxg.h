@@ -118,9 +118,10 @@ typedef struct hmxg_info {
 
 /* One launch of the per-evaluation launch sequence (SURVEY §7.3 / DESIGN.md):
  * kind 0 gather, 1 upward (level = subtree height), 2 far+downward (level = depth),
- * 3 near+leaf-downward, 4 scatter, 5 the whole-evaluation DAG launch, 6 near field alone
- * (the split leaf variant of narrow column counts) (every GEMM tile of
- * every level; the default sequence is gather, DAG, scatter). Byte/flop fields are ALGORITHMIC (each operand block
+ * 3 near+leaf-downward (level = wave with HMXG_UPLOAD_NEAR_ON_THE_FLY), 4 scatter, 5 the
+ * whole-evaluation DAG launch (every GEMM tile of every level; the default sequence is
+ * gather, DAG, scatter), 6 near field alone (the split leaf variant of narrow column counts),
+ * 7 near blocks generated into the scratch (on the fly; level = wave). Byte/flop fields are ALGORITHMIC (each operand block
  * counted once): the roofline numerators of bench.py. last_ms is the device time of that
  * launch in the last evaluation run with HMXG_F_TIME_PHASES on device 0. */
 typedef struct hmxg_phase {
@@ -234,6 +235,18 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
  * B_ij = K(skeleton_i, skeleton_j) (compress.cpp:139-142), and cds.bgen is ignored. */
 int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
                           double h, const uint64_t* skel_ptr, const uint32_t* skel_idx, hmxg_mat** out);
+
+/* hmxg_upload_generated with flags. HMXG_UPLOAD_NEAR_ON_THE_FLY: the near blocks are never
+ * resident. Every evaluation generates them from the points into a bounded scratch region of
+ * the tiles (HMXG_NEAR_SCRATCH_MB, default 2048), wave by wave: the leaf rows run in waves of
+ * leaf tasks whose near blocks fit it, each right after its blocks are generated. The
+ * resident CDS drops by |D| (cfg5 H2-b: 18.6 GB) for one generation of every near element
+ * per evaluation (its FP64 cost is ~Q/50 of the D products it feeds). Results are
+ * bit-identical to hmxg_upload_generated. Single device per context entry; no split. */
+#define HMXG_UPLOAD_NEAR_ON_THE_FLY 1u
+int hmxg_upload_generated_ex(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d,
+                             int32_t kernel, double h, const uint64_t* skel_ptr, const uint32_t* skel_idx,
+                             unsigned flags, hmxg_mat** out);
 
 /* Launch sequence description; phase_get synchronizes the timing events of the last
  * HMXG_F_TIME_PHASES evaluation before filling last_ms. */

@@ -25,7 +25,9 @@ HMXG_F_NO_SYNC = 0x2
 HMXG_F_TIME_PHASES = 0x4
 HMXG_F_NO_GRAPH = 0x8
 HMXG_F_LEVEL_LAUNCHES = 0x10
-PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter", 5: "dag", 6: "near"}
+PHASE_KINDS = {0: "gather", 1: "upward", 2: "far+downward", 3: "near+leaf", 4: "scatter", 5: "dag", 6: "near",
+               7: "near-gen"}
+HMXG_UPLOAD_NEAR_ON_THE_FLY = 1
 
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
@@ -199,6 +201,8 @@ HMXG_SYMBOLS = {
     ),
     "hmxg_upload_generated": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_void_p, C.c_uint32, C.c_int32,
                                         C.c_double, C.POINTER(C.c_uint64), _u32p, C.POINTER(C.c_void_p)]),
+    "hmxg_upload_generated_ex": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_void_p, C.c_uint32, C.c_int32,
+                                           C.c_double, C.POINTER(C.c_uint64), _u32p, C.c_uint, C.POINTER(C.c_void_p)]),
     "hmxg_upload_split": (C.c_int, [C.c_void_p, C.POINTER(CdsView), C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "hmxg_split_stage": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p,
                                    C.c_size_t, C.c_void_p]),

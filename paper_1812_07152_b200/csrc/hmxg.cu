@@ -104,6 +104,23 @@ struct DevState {
   // host staging of host-buffer collectives (hmxg_comm::host_buffers)
   unsigned char* comm_host = nullptr;
   std::size_t comm_host_bytes = 0;
+  // on-the-fly near field (Plan::near_otf): the points, the kernel, every wave's near chunks
+  // (GenChunk, concatenated) and the waves of leaf tasks whose chunks fit the scratch region
+  double* pts = nullptr;
+  KernelParams kp{};
+  GenChunk* gen_chunks = nullptr;
+  struct Wave {
+    std::uint32_t t0, t1;  // leaf tasks
+    std::uint64_t c0, c1;  // their chunks in gen_chunks
+  };
+  std::vector<Wave> waves;
+  std::vector<double> wave_flops, wave_io;  // per wave: executed flops and B/C bytes per column
+  // the last evaluation's launch sequence (hmxg_phase_count / hmxg_phase_get)
+  struct LaunchDesc {
+    std::uint32_t kind, level, tiles;
+    double flops_per_col, gen_bytes, io_bytes_per_col;
+  };
+  std::vector<LaunchDesc> launch_desc, gdesc;  // (gdesc: the cached graph's)
   // CTree program (ctree_csize): work units by level, built on first use
   unsigned char* ct_blob = nullptr;  // tasks, then segments at ct_segs_off
   std::uint32_t* ct_units = nullptr;
@@ -213,6 +230,11 @@ struct DevState {
     cudaFree(ct_blob);
     ct_units = ct_lvl = nullptr;
     ct_blob = nullptr;
+    cudaFree(pts);
+    cudaFree(gen_chunks);
+    pts = nullptr;
+    gen_chunks = nullptr;
+    waves.clear();
     ct_nlev = 0;
     cudaFreeHost(comm_host);
     comm_host = nullptr;
@@ -304,7 +326,7 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 #endif
 std::uint32_t ctree_csize(const Plan& plan, std::size_t q, unsigned grid);
 bool split_leaf(const Plan& plan, std::size_t q, unsigned grid) {
-  if (plan.split_phases.empty()) return false;
+  if (plan.split_phases.empty() || plan.near_otf) return false;  // on-the-fly near field: combined tasks
   if (ctree_csize(plan, q, grid)) return true;  // the CTree's leaf rows accumulate onto the near tiles
   std::uint64_t tasks = 0;
   for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
@@ -356,7 +378,7 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
   for (const Phase& ph : plan.phases) {
     if (ph.stage != stage) continue;
     if (ph.kind == kPhaseLeaf) {
-      if (!split) leaf.push_back(&ph);
+      if (!split && !plan.near_otf) leaf.push_back(&ph);  // on the fly: the leaf rows run in waves
     } else {
       tree.push_back(&ph);
     }
@@ -419,7 +441,8 @@ std::size_t dag_done_words(const Plan& plan, std::size_t q, std::uint32_t cstrid
 #define HMXG_FUSED_MAX_ELEMS (1u << 22)
 #endif
 bool fused_io(const Plan& plan, std::size_t q) {
-  return plan.nparts == 1 && plan.n * q <= std::uint64_t(HMXG_FUSED_MAX_ELEMS) && std::getenv("HMXG_NO_FUSED") == nullptr;
+  return plan.nparts == 1 && !plan.near_otf && plan.n * q <= std::uint64_t(HMXG_FUSED_MAX_ELEMS) &&
+         std::getenv("HMXG_NO_FUSED") == nullptr;
 }
 
 // CTree mode (kernels.cuh, ct_run; opt-in with HMXG_CTREE=1): small fused problems whose tree
@@ -729,6 +752,16 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       HMXG_CUDA(cudaEventRecordWithFlags(d.phase_ev[ev++], st, capturing ? cudaEventRecordExternal : 0u));
     return HMXG_OK;
   };
+  // the launch sequence as hmxg_phase_get reports it (algorithmic flops / bytes per launch)
+  std::vector<DevState::LaunchDesc> descs;
+  auto desc = [&](std::uint32_t kind, std::uint32_t level, std::uint32_t tiles, double flops, double gen, double io) {
+    descs.push_back(DevState::LaunchDesc{kind, level, tiles, flops, gen, io});
+  };
+  auto desc_phase = [&](const Phase& ph) {
+    desc(ph.kind == kPhaseUp ? 1u : (ph.kind == kPhaseDown ? 2u : (ph.kind == kPhaseLeaf ? 3u : 6u)), ph.level,
+         ph.task_end - ph.task_begin, ph.flops_per_col, ph.gen_bytes, ph.io_bytes_per_col);
+  };
+  auto desc_perm = [&](std::uint32_t kind) { desc(kind, 0, static_cast<std::uint32_t>((plan.n + 31) / 32), 0.0, 4.0 * plan.n, 16.0 * plan.n); };
   CUtensorMap tm_wp, tm_t, tm_s;
   const std::uint64_t ldq = d.cap_q;
   if (d.poison) {  // debug race detector: every live workspace row NaN before the launches
@@ -757,6 +790,36 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   p.segs = d.segs;
   p.idmap = d.idmap;
   p.q = qq;
+  // on-the-fly near field: every wave generates its near chunks into the scratch, then runs
+  // its leaf rows (the grouped GEMM over the wave's combined leaf tasks)
+  auto run_waves = [&](std::uint32_t* counters) -> int {
+    if (d.waves.empty()) return HMXG_OK;
+    HMXG_CUDA(cudaMemsetAsync(counters, 0, d.waves.size() * sizeof(std::uint32_t), st));
+    const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
+    for (std::size_t w = 0; w < d.waves.size(); ++w) {
+      const DevState::Wave& wv = d.waves[w];
+      const std::uint64_t nch = wv.c1 - wv.c0;
+      if (nch) {
+        gen_near<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 148ull * 16)), 256, 0, st>>>(
+            d.pts, d.kp, d.pmap, d.gen_chunks + wv.c0, nch, d.tiles);
+        ++*launches;
+        desc(7, static_cast<std::uint32_t>(w), static_cast<std::uint32_t>(nch), 0.0, 8.0 * kChunkElems * nch, 0.0);
+        HMXG_TRY(mark());
+      }
+      GemmParams pw = p;
+      pw.tasks = d.tasks + wv.t0;
+      const std::uint32_t ntasks = wv.t1 - wv.t0;
+      const std::uint64_t tiles = std::uint64_t(ntasks) * col_blocks;
+      if (tiles > 0xfffff000ull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many output tiles");
+      grouped_gemm<<<static_cast<unsigned>(std::min<std::uint64_t>(tiles, d.gemm_grid)), kThreads, kSmemBytes, st>>>(
+          tm_wp, tm_t, tm_s, pw, ntasks, counters + w);
+      ++*launches;
+      desc(3, static_cast<std::uint32_t>(w), ntasks, d.wave_flops[w], 4.0 * d.wave_flops[w], d.wave_io[w]);
+      HMXG_TRY(mark());
+    }
+    HMXG_CUDA(cudaGetLastError());
+    return HMXG_OK;
+  };
   if (!levels) {
     const DevState::DagItems* di = nullptr;
     const bool ct = ctree_csize(plan, q, d.gemm_grid) != 0;
@@ -849,6 +912,17 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       }
       ++*launches;
       HMXG_TRY(mark());
+      {  // the permutations ran inside: W read and Y written once more per column
+        DevState::LaunchDesc a{5, 0, 0, 0.0, 4.0 * plan.n, 16.0 * plan.n};
+        for (const Phase* ph : level_phases(plan, q, d.gemm_grid)) {
+          a.tiles += ph->task_end - ph->task_begin;
+          a.flops_per_col += ph->flops_per_col;
+          a.gen_bytes += ph->gen_bytes;
+          a.io_bytes_per_col += ph->io_bytes_per_col;
+        }
+        descs.push_back(a);
+      }
+      d.launch_desc = std::move(descs);
       HMXG_CUDA(cudaGetLastError());
       d.counters_dirty = false;
       d.last_launches = 1;
@@ -863,21 +937,36 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     // normally, so each event brackets one kernel. permute_out zeroes the DAG's counters.
     permute_in<<<pgrid2, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, nullptr, 0);
     ++*launches;
+    desc_perm(0);
     HMXG_TRY(mark());
     const bool pdl = !time_phases;  // an event between two kernels would break the programmatic edge
     const bool narrow = dp.colsplit > 1 || dp.cstride > 1;
-    HMXG_TRY(launch_dependent(pdl, narrow ? eval_dag<true> : eval_dag<false>, dim3(grid), dim3(kThreads), kSmemBytes,
-                              st, tm_wp, tm_t, tm_s, p, dp));
+    if (grid) {  // (on the fly, a tree without levels has nothing for the DAG)
+      HMXG_TRY(launch_dependent(pdl, narrow ? eval_dag<true> : eval_dag<false>, dim3(grid), dim3(kThreads), kSmemBytes,
+                                st, tm_wp, tm_t, tm_s, p, dp));
+      ++*launches;
+      DevState::LaunchDesc a{5, 0, 0, 0.0, 0.0, 0.0};
+      for (const Phase* ph : level_phases(plan, q, d.gemm_grid)) {
+        if (plan.near_otf && ph->kind == kPhaseLeaf) continue;  // the waves below
+        a.tiles += ph->task_end - ph->task_begin;
+        a.flops_per_col += ph->flops_per_col;
+        a.gen_bytes += ph->gen_bytes;
+        a.io_bytes_per_col += ph->io_bytes_per_col;
+      }
+      descs.push_back(a);
+      HMXG_TRY(mark());
+    }
+    if (plan.near_otf) HMXG_TRY(run_waves(d.tile_counters));
+    HMXG_TRY(launch_dependent(pdl && !plan.near_otf, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp),
+                              std::uint64_t(ldq), static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n,
+                              qq, d.dag_done, std::uint64_t(words + 1)));
     ++*launches;
+    desc_perm(4);
     HMXG_TRY(mark());
-    HMXG_TRY(launch_dependent(pdl, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp), std::uint64_t(ldq),
-                              static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n, qq, d.dag_done,
-                              std::uint64_t(words + 1)));
-    ++*launches;
-    HMXG_TRY(mark());
+    d.launch_desc = std::move(descs);
     HMXG_CUDA(cudaGetLastError());
     d.counters_dirty = false;
-    d.last_launches = 3;
+    d.last_launches = static_cast<std::uint32_t>(d.launch_desc.size());
     if (time_phases) d.phase_valid = true;
     return HMXG_OK;
   }
@@ -887,12 +976,17 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
   if (pgrid.y > 65535) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many columns for one call");
   permute_in<<<pgrid, eblk, 0, st>>>(w, ldw, d.ipmap, d.wp, ldq, n, qq, nullptr, 0);
   ++*launches;
+  desc_perm(0);
   HMXG_TRY(mark());
   const std::uint32_t col_blocks = (qq + kBN - 1) / kBN;
   const std::vector<const Phase*> lphases = level_phases(plan, q, d.gemm_grid);
   HMXG_CUDA(cudaMemsetAsync(d.tile_counters, 0, lphases.size() * sizeof(std::uint32_t), st));
   for (std::size_t ph_i = 0; ph_i < lphases.size(); ++ph_i) {
     const Phase& ph = *lphases[ph_i];
+    if (plan.near_otf && ph.kind == kPhaseLeaf) {
+      HMXG_TRY(run_waves(d.tile_counters + lphases.size()));
+      continue;
+    }
     p.tasks = d.tasks + ph.task_begin;
     const std::uint32_t ntasks = ph.task_end - ph.task_begin;
     const std::uint64_t tiles = std::uint64_t(ntasks) * col_blocks;
@@ -900,12 +994,15 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(tiles, d.gemm_grid));
     grouped_gemm<<<grid, kThreads, kSmemBytes, st>>>(tm_wp, tm_t, tm_s, p, ntasks, d.tile_counters + ph_i);
     ++*launches;
+    desc_phase(ph);
     HMXG_TRY(mark());
   }
   permute_out<<<pgrid, eblk, 0, st>>>(d.yp, ldq, d.ipmap, y, ldy, n, qq, nullptr, 0);
   ++*launches;
-  d.last_launches = static_cast<std::uint32_t>(lphases.size() + 2);
+  desc_perm(4);
   HMXG_TRY(mark());
+  d.launch_desc = std::move(descs);
+  d.last_launches = static_cast<std::uint32_t>(d.launch_desc.size());
   HMXG_CUDA(cudaGetLastError());
   if (time_phases) d.phase_valid = true;
   return HMXG_OK;
@@ -1135,16 +1232,16 @@ int generate_blocks(const double* pts, const KernelParams& kp, const std::vector
 
 // dgen (and, with skeletons, bgen) on the device from the points.
 int generate_generators(const hmxg_cds_view& v, const Plan& plan, const NearSource& src, double** gd, double** gb,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool near = true) {
   double* pts = nullptr;
   HMXG_TRY(dev_upload(&pts, src.coords, v.n * src.d, st));
-  std::vector<GenBlock> blocks(v.num_near);
-  for (std::uint64_t s = 0; s < v.num_near; ++s) {
+  std::vector<GenBlock> blocks(near ? v.num_near : 0);
+  for (std::uint64_t s = 0; s < blocks.size(); ++s) {
     const std::uint32_t i = v.near_pairs[2 * s], j = v.near_pairs[2 * s + 1];
     blocks[s] = GenBlock{v.dptr[s], v.start[i], v.start[j], v.end[i] - v.start[i], v.end[j] - v.start[j]};
   }
   const std::vector<std::uint32_t> perm(v.perm, v.perm + v.n);
-  int rc = generate_blocks(pts, src.kp, perm, blocks, plan.d_elems, gd, st);
+  int rc = near ? generate_blocks(pts, src.kp, perm, blocks, plan.d_elems, gd, st) : HMXG_OK;
   if (rc == HMXG_OK && src.skel_ptr) {
     blocks.assign(v.num_far, GenBlock{});
     for (std::uint64_t s = 0; s < v.num_far; ++s) {
@@ -1158,8 +1255,92 @@ int generate_generators(const hmxg_cds_view& v, const Plan& plan, const NearSour
   return rc;
 }
 
+// On-the-fly near field (HMXG_UPLOAD_NEAR_ON_THE_FLY): the resident tiles hold every A chunk
+// but the near blocks' (compacted), then a scratch region. The combined leaf tasks are cut
+// into waves whose near chunks fit it, in task order; their near segments point into the
+// scratch at wave-relative offsets, and every evaluation generates a wave's chunks (gen_near)
+// right before the wave's leaf rows run.
+struct OtfLayout {
+  std::vector<SegDev> segs;         // plan.segs, tile offsets re-based
+  std::vector<TileSrc> srcs;        // plan.tile_src, tile offsets re-based (near ones unused)
+  std::vector<std::uint32_t> cseg;  // resident chunk -> segment
+  std::uint64_t resident_elems = 0, scratch_elems = 0;
+  std::vector<GenChunk> chunks;
+  std::vector<DevState::Wave> waves;
+  std::vector<double> wave_flops_per_col, wave_io_per_col;
+};
+#ifndef HMXG_NEAR_SCRATCH_MB
+#define HMXG_NEAR_SCRATCH_MB 2048
+#endif
+int otf_layout(const Plan& plan, OtfLayout& L) {
+  std::uint64_t scratch_bytes = std::uint64_t(HMXG_NEAR_SCRATCH_MB) << 20;
+  if (const char* e = std::getenv("HMXG_NEAR_SCRATCH_MB")) scratch_bytes = std::uint64_t(std::max(1, std::atoi(e))) << 20;
+  const std::size_t ns = plan.segs.size();
+  L.segs = plan.segs;
+  L.srcs = plan.tile_src;
+  std::vector<std::uint8_t> is_d(ns, 0), placed(ns, 0);
+  std::uint64_t off = 0;
+  for (std::size_t s = 0; s < ns; ++s) {
+    is_d[s] = plan.tile_src[s].gen == kGenD;
+    if (is_d[s]) continue;
+    L.segs[s].tile_off = off;
+    L.srcs[s].tile_off = off;
+    for (std::uint32_t c = 0; c < plan.segs[s].nchunks; ++c) L.cseg.push_back(static_cast<std::uint32_t>(s));
+    off += std::uint64_t(plan.segs[s].nchunks) * kChunkElems;
+  }
+  L.resident_elems = off;
+  const Phase* leaf = nullptr;
+  for (const Phase& ph : plan.phases)
+    if (ph.kind == kPhaseLeaf && ph.stage == 0) leaf = &ph;
+  if (!leaf) return HMXG_OK;
+  auto dchunks = [&](std::uint32_t t) {
+    std::uint64_t c = 0;
+    for (std::uint32_t si = plan.tasks[t].seg_begin; si < plan.tasks[t].seg_end; ++si)
+      if (is_d[si]) c += plan.segs[si].nchunks;
+    return c;
+  };
+  std::uint64_t cap = std::max<std::uint64_t>(1, scratch_bytes / (kChunkElems * sizeof(double)));
+  for (std::uint32_t t = leaf->task_begin; t < leaf->task_end; ++t) cap = std::max(cap, dchunks(t));
+  std::uint32_t t = leaf->task_begin;
+  while (t < leaf->task_end) {
+    DevState::Wave w{t, t, L.chunks.size(), 0};
+    std::uint64_t woff = 0;  // chunks of the wave so far
+    double flops = 0.0, io = 0.0;
+    while (t < leaf->task_end && (w.t1 == w.t0 || woff + dchunks(t) <= cap)) {
+      const Task& tk = plan.tasks[t];
+      for (std::uint32_t si = tk.seg_begin; si < tk.seg_end; ++si) {
+        const TileSrc& ts = plan.tile_src[si];
+        flops += 2.0 * ts.m * ts.k;
+        io += 8.0 * ts.k / std::max<std::uint32_t>(1, plan.yp_tiles[tk.node]);
+        if (!is_d[si]) continue;
+        if (placed[si]++) return set_err(HMXG_EINVAL, "internal: a near segment in two leaf tasks");
+        const std::uint64_t base = L.resident_elems / kChunkElems + woff;
+        L.segs[si].tile_off = base * kChunkElems;
+        for (std::uint32_t c = 0; c < plan.segs[si].nchunks; ++c) {
+          GenChunk g{};
+          g.out = base + c;
+          g.yrow = tk.c_row;
+          g.brow = plan.segs[si].b_row + c * kBK;
+          g.m = ts.m;
+          g.kvalid = static_cast<std::uint16_t>(std::min<std::uint64_t>(kBK, ts.k - std::uint64_t(c) * kBK));
+          L.chunks.push_back(g);
+        }
+        woff += plan.segs[si].nchunks;
+      }
+      io += 8.0 * tk.m;
+      w.t1 = ++t;
+    }
+    w.c1 = L.chunks.size();
+    L.scratch_elems = std::max(L.scratch_elems, woff * kChunkElems);
+    L.waves.push_back(w);
+    L.wave_flops_per_col.push_back(flops);
+    L.wave_io_per_col.push_back(io);
+  }
+  return HMXG_OK;
+}
+
 int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split, hmxg_mat** out,
-                const NearSource* near_src = nullptr) {
+                const NearSource* near_src = nullptr, bool otf = false) {
   if (!ctx || !cds || !out) return set_err(HMXG_EINVAL, "hmxg_upload: null argument");
   if (near_src && split.nparts > 1) return set_err(HMXG_EINVAL, "hmxg_upload: generated near field is single-part");
   *out = nullptr;
@@ -1167,6 +1348,12 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
   mat->ctx = ctx;
   std::string err;
   if (!build_plan(*cds, kBM, mat->plan, err, split)) return set_err(HMXG_EINVAL, err);
+  OtfLayout otf_l;
+  if (otf) {
+    if (!near_src || split.nparts != 1) return set_err(HMXG_EINVAL, "hmxg_upload: near field on the fly needs points");
+    mat->plan.near_otf = true;
+    HMXG_TRY(otf_layout(mat->plan, otf_l));
+  }
   const double* gsrc[3] = {cds->dgen, cds->bgen, cds->vgen};
   std::vector<double> gcompact[3];
   if (split.nparts > 1) HMXG_TRY(compact_generators(*cds, mat->plan, gsrc, gcompact));
@@ -1182,7 +1369,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
         HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     HMXG_CUDA(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
-    d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3);
+    d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3 + 2 * otf_l.waves.size());
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     HMXG_CUDA(cudaFuncSetAttribute(eval_dag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -1202,29 +1389,41 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
 #define HMXG_GEMM_CTAS_PER_SM 3
 #endif
       d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
-      HMXG_CUDA(cudaMalloc(&d.tile_counters,
-                           std::max<std::size_t>(1, plan.phases.size() + plan.split_phases.size()) * sizeof(std::uint32_t)));
+      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size() + plan.split_phases.size() +
+                                                                          otf_l.waves.size()) * sizeof(std::uint32_t)));
     }
     // raw generators -> pre-tiled A operands on the device, then the raw copies go away
     double *gd = nullptr, *gb = nullptr, *gv = nullptr;
     TileSrc* srcs = nullptr;
     std::uint32_t* cseg = nullptr;
     if (near_src)
-      HMXG_TRY(generate_generators(*cds, plan, *near_src, &gd, &gb, d.comp));
+      HMXG_TRY(generate_generators(*cds, plan, *near_src, &gd, &gb, d.comp, /*near=*/!otf));
     else
       HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
     if (!near_src || !near_src->skel_ptr) HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
     HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
-    HMXG_TRY(dev_upload(&srcs, plan.tile_src.data(), plan.tile_src.size(), d.comp));
-    HMXG_TRY(dev_upload(&cseg, plan.chunk_seg.data(), plan.chunk_seg.size(), d.comp));
+    const std::vector<TileSrc>& tsrc = otf ? otf_l.srcs : plan.tile_src;
+    const std::vector<std::uint32_t>& tcseg = otf ? otf_l.cseg : plan.chunk_seg;
+    const std::uint64_t tile_elems = otf ? otf_l.resident_elems + otf_l.scratch_elems : plan.tile_elems;
+    HMXG_TRY(dev_upload(&srcs, tsrc.data(), tsrc.size(), d.comp));
+    HMXG_TRY(dev_upload(&cseg, tcseg.data(), tcseg.size(), d.comp));
     std::uint32_t* maps = nullptr;
     HMXG_TRY(dev_upload(&maps, plan.maps.data(), plan.maps.size(), d.comp));
-    if (plan.tile_elems) {
-      HMXG_CUDA(cudaMalloc(&d.tiles, plan.tile_elems * sizeof(double)));
-      const std::uint64_t nch = plan.chunk_seg.size();
-      tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
-                                                                                               maps, d.tiles, nch);
+    if (tile_elems) {
+      HMXG_CUDA(cudaMalloc(&d.tiles, tile_elems * sizeof(double)));
+      const std::uint64_t nch = tcseg.size();
+      if (nch)
+        tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
+                                                                                                 maps, d.tiles, nch);
       HMXG_CUDA(cudaGetLastError());
+    }
+    if (otf) {  // the points and every wave's near chunks; the near blocks themselves never exist
+      HMXG_TRY(dev_upload(&d.pts, near_src->coords, cds->n * near_src->d, d.comp));
+      HMXG_TRY(dev_upload(&d.gen_chunks, otf_l.chunks.data(), otf_l.chunks.size(), d.comp));
+      d.kp = near_src->kp;
+      d.waves = otf_l.waves;
+      d.wave_flops = otf_l.wave_flops_per_col;
+      d.wave_io = otf_l.wave_io_per_col;
     }
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
     cudaFree(gd);
@@ -1234,7 +1433,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     cudaFree(cseg);
     cudaFree(maps);
     HMXG_TRY(dev_upload(&d.tasks, plan.tasks.data(), plan.tasks.size(), d.comp));
-    HMXG_TRY(dev_upload(&d.segs, plan.segs.data(), plan.segs.size(), d.comp));
+    HMXG_TRY(dev_upload(&d.segs, otf ? otf_l.segs.data() : plan.segs.data(), plan.segs.size(), d.comp));
     HMXG_TRY(dev_upload(&d.idmap, plan.idmap.data(), plan.idmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.ipmap, plan.ipmap.data(), plan.ipmap.size(), d.comp));
     HMXG_TRY(dev_upload(&d.node_tiles, plan.node_tiles.data(), plan.node_tiles.size(), d.comp));
@@ -1264,7 +1463,8 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       }
     }
     HMXG_CUDA(cudaStreamSynchronize(d.comp));
-    d.resident_bytes = 8 * plan.tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
+    d.resident_bytes = 8 * tile_elems + sizeof(Task) * plan.tasks.size() + sizeof(SegDev) * plan.segs.size() +
+                       (otf ? 8 * cds->n * near_src->d + sizeof(GenChunk) * otf_l.chunks.size() : 0) +
                        4 * plan.ipmap.size() + 4 * plan.idmap.size();
   }
   *out = mat.release();
@@ -1737,6 +1937,13 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
 
 int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
                           double h, const uint64_t* skel_ptr, const uint32_t* skel_idx, hmxg_mat** out) {
+  return hmxg_upload_generated_ex(ctx, cds, coords, d, kernel, h, skel_ptr, skel_idx, 0u, out);
+}
+
+int hmxg_upload_generated_ex(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d,
+                             int32_t kernel, double h, const uint64_t* skel_ptr, const uint32_t* skel_idx,
+                             unsigned flags, hmxg_mat** out) {
+  if (flags & ~HMXG_UPLOAD_NEAR_ON_THE_FLY) return set_err(HMXG_EINVAL, "hmxg_upload_generated_ex: unknown flags");
   if (!cds || !coords || d == 0) return set_err(HMXG_EINVAL, "hmxg_upload_generated: null points");
   if (skel_ptr) {  // every node's skeleton must have its srank entries, all of them points
     if (cds->num_nodes && !cds->sranks) return set_err(HMXG_EINVAL, "cds: null array in view");
@@ -1762,7 +1969,7 @@ int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double*
   SplitSpec spec;
   spec.generated_near = true;
   spec.generated_far = skel_ptr != nullptr;
-  return upload_impl(ctx, cds, spec, out, &src);
+  return upload_impl(ctx, cds, spec, out, &src, (flags & HMXG_UPLOAD_NEAR_ON_THE_FLY) != 0);
 }
 
 int hmxg_upload_split(hmxg_ctx* ctx, const hmxg_cds_view* cds, uint32_t nparts, uint32_t part, hmxg_mat** out) {
@@ -1903,47 +2110,20 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
 // eval_dag, permute-out) by default, the level sequence after HMXG_F_LEVEL_LAUNCHES.
 int hmxg_phase_count(const hmxg_mat* mat) {
   if (!mat) return -1;
-  const DevState& d = mat->devs[0];
-  return d.last_levels ? static_cast<int>(level_phases(mat->plan, d.last_q, d.gemm_grid).size() + 2)
-                       : (d.last_fused ? 1 : 3);
+  return static_cast<int>(mat->devs[0].launch_desc.size());
 }
 
 int hmxg_phase_get(hmxg_mat* mat, uint32_t idx, hmxg_phase* out) {
   if (!mat || !out) return set_err(HMXG_EINVAL, "hmxg_phase_get: null argument");
-  const Plan& p = mat->plan;
-  const bool levels = mat->devs[0].last_levels;
-  const bool fused = !levels && mat->devs[0].last_fused;
-  const std::vector<const Phase*> lphases = level_phases(p, mat->devs[0].last_q, mat->devs[0].gemm_grid);
-  const std::uint32_t count = static_cast<std::uint32_t>(levels ? lphases.size() + 2 : (fused ? 1 : 3));
-  if (idx >= count) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
+  const std::vector<DevState::LaunchDesc>& ld = mat->devs[0].launch_desc;
+  if (idx >= ld.size()) return set_err(HMXG_EINVAL, "hmxg_phase_get: index out of range");
   std::memset(out, 0, sizeof *out);
-  if (fused || (!levels && idx == 1)) {  // the whole-evaluation DAG launch: every GEMM tile
-    out->kind = 5;
-    for (const Phase* php : lphases) {
-      const Phase& ph = *php;
-      out->tiles += ph.task_end - ph.task_begin;
-      out->flops_per_col += ph.flops_per_col;
-      out->gen_bytes += ph.gen_bytes;
-      out->io_bytes_per_col += ph.io_bytes_per_col;
-    }
-    if (fused) {  // the permutations ran inside: W read and Y written once more per column
-      out->io_bytes_per_col += 16.0 * p.n;
-      out->gen_bytes += 4.0 * p.n;
-    }
-  } else if (idx == 0 || idx + 1 == count) {  // permutation kernels: read n, write n per column
-    out->kind = idx == 0 ? 0 : 4;
-    out->tiles = static_cast<std::uint32_t>((p.n + 31) / 32);
-    out->io_bytes_per_col = 16.0 * p.n;
-    out->gen_bytes = 4.0 * p.n;  // the permutation itself
-  } else {
-    const Phase& ph = *lphases[idx - 1];
-    out->kind = ph.kind == kPhaseUp ? 1 : (ph.kind == kPhaseDown ? 2 : (ph.kind == kPhaseLeaf ? 3 : 6));
-    out->level = ph.level;
-    out->tiles = ph.task_end - ph.task_begin;
-    out->flops_per_col = ph.flops_per_col;
-    out->gen_bytes = ph.gen_bytes;
-    out->io_bytes_per_col = ph.io_bytes_per_col;
-  }
+  out->kind = ld[idx].kind;
+  out->level = ld[idx].level;
+  out->tiles = ld[idx].tiles;
+  out->flops_per_col = ld[idx].flops_per_col;
+  out->gen_bytes = ld[idx].gen_bytes;
+  out->io_bytes_per_col = ld[idx].io_bytes_per_col;
   DevState& d = mat->devs[0];
   if (d.phase_valid) {
     HMXG_CUDA(cudaSetDevice(d.dev));
@@ -2013,11 +2193,13 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
         d.gkey = key;
         d.glaunches = captured;
         d.gfused = d.last_fused;
+        d.gdesc = d.launch_desc;
       }
       HMXG_CUDA(cudaGraphLaunch(d.gexec, st));
       launches += d.glaunches;
       d.phase_valid = time_phases;  // the graph's event nodes time this replay
       d.last_fused = d.gfused;      // and the launch sequence is the captured one
+      d.launch_desc = d.gdesc;
       d.last_launches = d.glaunches;
       d.last_q = q;
     }

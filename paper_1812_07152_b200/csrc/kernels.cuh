@@ -218,6 +218,42 @@ __global__ void __launch_bounds__(256) gen_blocks(const double* __restrict__ pts
   }
 }
 
+// ---------------------------------------------------------------- near field on the fly
+// One pre-tiled A chunk of a near block (hmxg_upload_generated_ex, HMXG_UPLOAD_NEAR_ON_THE_FLY):
+// element (r, k) = K(x_{pmap[yrow + r]}, x_{pmap[brow + k]}) for r < m, k < kvalid, else 0 --
+// the tile's Yp row r and the B chunk's Wp row k name the two points (the leaf row orders of
+// the identity-row lowering included), so it equals tile_a's chunk of the block that
+// gen_blocks generates at upload, bit for bit (same kernel_value, same argument order).
+struct GenChunk {
+  std::uint64_t out;   // chunk index in the tiles array (the scratch region)
+  std::uint32_t yrow;  // Yp row of tile row 0
+  std::uint32_t brow;  // Wp row of k = 0
+  std::uint16_t m, kvalid;
+  std::uint32_t pad;
+};
+static_assert(sizeof(GenChunk) == 24, "GenChunk layout");
+
+// A wave's near-field chunks into the scratch region of the tiles (one launch per wave, before
+// the wave's leaf rows): consecutive threads write consecutive (swizzled) rows of a chunk.
+__global__ void __launch_bounds__(256) gen_near(const double* __restrict__ pts, const KernelParams kp,
+                                                const std::uint32_t* __restrict__ pmap,
+                                                const GenChunk* __restrict__ chunks, std::uint64_t nchunks,
+                                                double* __restrict__ tiles) {
+  for (std::uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const GenChunk g = chunks[c];
+    double* out = tiles + g.out * 1024u;
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int r = e & 63, k = e >> 6;
+      double v = 0.0;
+      if (r < g.m && k < g.kvalid) {
+        const std::uint64_t pi = __ldg(pmap + g.yrow + r), pj = __ldg(pmap + g.brow + k);
+        v = kernel_value(kp, pts + pi * kp.d, pts + pj * kp.d);
+      }
+      out[k * 64 + (r ^ ((k & 3) << 2))] = v;  // a_swz(k, r)
+    }
+  }
+}
+
 // ---------------------------------------------------------------- A pre-tiling
 __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
                        const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,

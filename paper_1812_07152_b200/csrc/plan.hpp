@@ -160,6 +160,7 @@ struct Plan {
   std::vector<std::uint32_t> maps;
   std::vector<std::uint32_t> idmap;
   double identity_flops_per_col = 0.0;  // multiply-adds by exact 0/1 rows the kernel skips
+  bool near_otf = false;                 // near blocks generated per evaluation (hmxg_upload_generated_ex)
   mutable double ct_dmma = -1.0;         // CTree work per 8-column octet in DMMAs (hmxg.cu, cached)
   mutable std::uint64_t ct_smem = 0;     // its tables' shared-memory bytes
 };

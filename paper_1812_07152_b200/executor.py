@@ -156,10 +156,12 @@ class Evaluator:
     """A CDS resident on the devices of a context (``hmxg_upload``)."""
 
     def __init__(self, cds: CDS, devices=(0,), context: Context | None = None, points: np.ndarray | None = None,
-                 kernel=None, skeletons: tuple[np.ndarray, np.ndarray] | None = None):
+                 kernel=None, skeletons: tuple[np.ndarray, np.ndarray] | None = None, near_on_the_fly: bool = False):
         """``points``/``kernel`` (an accuracy.Kernel): generate the near field on the device
         from the points (hmxg_upload_generated); the CDS's dgen is then not read. With
-        ``skeletons`` = (skel_ptr, skel_idx) (CSR over nodes) the far blocks are generated too."""
+        ``skeletons`` = (skel_ptr, skel_idx) (CSR over nodes) the far blocks are generated too.
+        ``near_on_the_fly``: the near blocks are never resident; every evaluation generates
+        them wave by wave into a bounded scratch (HMXG_UPLOAD_NEAR_ON_THE_FLY)."""
         self.cds = cds
         self.ctx = context or Context(devices)
         self._own_ctx = context is None
@@ -175,10 +177,11 @@ class Evaluator:
             if skeletons is not None:
                 sp = np.ascontiguousarray(skeletons[0], dtype=np.uint64)
                 si = np.ascontiguousarray(skeletons[1], dtype=np.uint32)
-            _check(N.hmxg().hmxg_upload_generated(
+            _check(N.hmxg().hmxg_upload_generated_ex(
                 self.ctx.handle, C.byref(v), pts.ctypes.data_as(C.c_void_p), pts.shape[1], kernel.code, kernel.h,
                 sp.ctypes.data_as(C.POINTER(C.c_uint64)) if sp is not None else None,
-                si.ctypes.data_as(N._u32p) if si is not None and si.size else None, C.byref(h)))
+                si.ctypes.data_as(N._u32p) if si is not None and si.size else None,
+                N.HMXG_UPLOAD_NEAR_ON_THE_FLY if near_on_the_fly else 0, C.byref(h)))
         self._h = h
         self._lock = threading.Lock()
 
