@@ -358,50 +358,88 @@ std::uint32_t colsplit(const Plan& plan, std::size_t q, unsigned grid, std::uint
   const std::uint64_t items = tasks * ((q + kBN - 1) / kBN);
   return items < grid ? 4u : (items < 4ull * grid ? 2u : 1u);
 }
+// Partial split of the leaf rows (wide DAGs): the near field of a fraction f of the leaves runs
+// as split-variant near items dealt out between the tree levels -- they depend on Wp only, so
+// they fill the slots the narrow upper levels leave idle -- and those leaves' V_i S_i rows
+// accumulate onto them at the end; the other leaves keep the combined tasks (no Yp round
+// trip). f = 1 is the split variant of narrow DAGs (split_leaf), f = 0 the combined one. Both
+// variants sum every row in one order, so any f gives the same bits. HMXG_SPLIT_FRAC sets f.
+#ifndef HMXG_SPLIT_FRAC
+#define HMXG_SPLIT_FRAC 0.0
+#endif
+double split_frac(const Plan& plan, std::size_t q, unsigned grid) {
+  if (plan.split_phases.empty() || plan.near_otf || plan.nparts != 1) return 0.0;
+  if (split_leaf(plan, q, grid)) return 1.0;
+  double f = HMXG_SPLIT_FRAC;
+  if (const char* e = std::getenv("HMXG_SPLIT_FRAC")) f = std::atof(e);
+  return std::min(1.0, std::max(0.0, f));
+}
+// Leaves whose rows run split for fraction f: among the leaves with near tiles and a basis
+// (those with an accumulating task), evenly spaced in task order.
+std::vector<std::uint8_t> split_set(const Plan& plan, double f) {
+  std::vector<std::uint8_t> sel(plan.num_nodes, 0);
+  if (f <= 0.0) return sel;
+  std::vector<std::uint32_t> cand;
+  for (const Phase& ph : plan.split_phases)
+    if (ph.kind == kPhaseLeaf && ph.stage == 0)
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+        if ((plan.tasks[t].flags & kTaskAccumulate) && (cand.empty() || cand.back() != plan.tasks[t].node))
+          cand.push_back(plan.tasks[t].node);
+  for (std::size_t k = 0; k < cand.size(); ++k)
+    if (f >= 1.0 || std::floor((k + 1) * f) > std::floor(k * f)) sel[cand[k]] = 1;
+  return sel;
+}
 std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage, unsigned grid) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
   const std::uint32_t S = colsplit(plan, q, grid, stage);
   std::vector<std::uint64_t> items;
-  auto emit = [&](std::uint32_t t0, std::uint32_t t1) {
-    for (std::uint32_t t = t0; t < t1; ++t)
-      for (std::uint32_t cb = 0; cb < ncb; ++cb)
-        for (std::uint32_t sub = 0; sub < S; ++sub) items.push_back(make_item(kItemGemm, cb, t, sub));
+  auto emit_task = [&](std::uint32_t t) {
+    for (std::uint32_t cb = 0; cb < ncb; ++cb)
+      for (std::uint32_t sub = 0; sub < S; ++sub) items.push_back(make_item(kItemGemm, cb, t, sub));
   };
-  const bool split = split_leaf(plan, q, grid);
+  auto emit = [&](std::uint32_t t0, std::uint32_t t1) {
+    for (std::uint32_t t = t0; t < t1; ++t) emit_task(t);
+  };
   if (stage == 0 && ctree_csize(plan, q, grid)) {  // CTree mode: the near tiles only
     for (const Phase& ph : plan.split_phases)
       if (ph.kind == kPhaseNear) emit(ph.task_begin, ph.task_end);
     return items;
   }
-  std::vector<const Phase*> tree, leaf;
-  const Phase* near = nullptr;
+  const double f = stage == 0 ? split_frac(plan, q, grid) : (split_leaf(plan, q, grid) ? 1.0 : 0.0);
+  const std::vector<std::uint8_t> sel = split_set(plan, f);
+  // tree phases; the leaf rows: combined tasks of the leaves not split, the near tasks and the
+  // accumulating tasks of the split ones (and every near task when f = 1: those of leaves
+  // without a basis are their final rows)
+  std::vector<const Phase*> tree;
+  std::vector<std::uint32_t> near, tail;
   for (const Phase& ph : plan.phases) {
     if (ph.stage != stage) continue;
-    if (ph.kind == kPhaseLeaf) {
-      if (!split && !plan.near_otf) leaf.push_back(&ph);  // on the fly: the leaf rows run in waves
-    } else {
+    if (ph.kind != kPhaseLeaf) {
       tree.push_back(&ph);
+    } else if (f < 1.0 && !plan.near_otf) {  // on the fly: the leaf rows run in waves
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+        if (!sel[plan.tasks[t].node]) tail.push_back(t);
     }
   }
-  if (split)
+  if (f > 0.0)
     for (const Phase& ph : plan.split_phases) {
       if (ph.stage != stage) continue;
-      if (ph.kind == kPhaseNear) near = &ph;
-      else leaf.push_back(&ph);
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+        if (f >= 1.0 || sel[plan.tasks[t].node]) (ph.kind == kPhaseNear ? near : tail).push_back(t);
     }
-  const std::uint64_t nt = near ? near->task_end - near->task_begin : 0;
+  const std::uint64_t nt = near.size();
   const std::size_t L = tree.size();
   const std::size_t nslices = L > 1 ? L - 1 : 1;  // after every level but the first
   for (std::size_t k = 0; k < L; ++k) {
     emit(tree[k]->task_begin, tree[k]->task_end);
-    if (near && (L == 1 || k >= 1)) {
+    if (nt && (L == 1 || k >= 1)) {
       const std::size_t slice = L == 1 ? 0 : k - 1;
-      emit(near->task_begin + static_cast<std::uint32_t>(nt * slice / nslices),
-           near->task_begin + static_cast<std::uint32_t>(nt * (slice + 1) / nslices));
+      for (std::uint64_t i = nt * slice / nslices; i < nt * (slice + 1) / nslices; ++i) emit_task(near[i]);
     }
   }
-  if (near && L == 0) emit(near->task_begin, near->task_end);
-  for (const Phase* ph : leaf) emit(ph->task_begin, ph->task_end);
+  if (nt && L == 0)
+    for (std::uint32_t t : near) emit_task(t);
+  for (std::uint32_t t : tail) emit_task(t);
   return items;
 }
 
@@ -838,7 +876,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     dp.cstride = cst;
     dp.node_tiles = d.node_tiles;
     dp.yp_tiles = d.yp_tiles;
-    dp.signal_yp = split_leaf(plan, q, d.gemm_grid) ? 1u : 0u;
+    dp.signal_yp = split_frac(plan, q, d.gemm_grid) > 0.0 ? 1u : 0u;
     dp.colsplit = colsplit(plan, q, d.gemm_grid);
     dp.ncb = (qq + kBN - 1) / kBN;
     dp.nodes = plan.num_nodes;
@@ -1849,21 +1887,26 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   const std::uint32_t ncb = static_cast<std::uint32_t>((q + kBN - 1) / kBN);
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
   if (nitems) *nitems = items.size();
-  const bool split = split_leaf(plan, q, grid);
+  const double f = split_frac(plan, q, grid);
+  const bool split = f > 0.0;  // (some) leaves run the split variant
+  const std::vector<std::uint8_t> sel = split_set(plan, f);
   const std::uint32_t S = colsplit(plan, q, grid);  // parts per tile: every tile appears S times
   if (ctree_csize(plan, q, grid)) return ct_check(plan, items, static_cast<std::uint32_t>(q), S);
-  // (1) every task of the variant that runs, once per column block
+  // (1) every task of the variant that runs, once per column block: the tree phases, the
+  // combined leaf tasks of the leaves not split, the near and accumulating tasks of the split
+  // ones (every near task when f = 1)
   std::vector<std::uint32_t> want(plan.tasks.size(), 0), seen(plan.tasks.size() * std::size_t(ncb), 0);
+  std::vector<std::uint8_t> is_near(plan.tasks.size(), 0);
   for (const Phase& ph : plan.phases)
-    if (!(split && ph.kind == kPhaseLeaf))
-      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) want[t] = 1;
+    for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+      if (ph.kind != kPhaseLeaf || (f < 1.0 && !sel[plan.tasks[t].node])) want[t] = 1;
   if (split)
     for (const Phase& ph : plan.split_phases)
-      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) want[t] = 1;
-  std::vector<std::uint8_t> is_near(plan.tasks.size(), 0);
-  for (const Phase& ph : plan.split_phases)
-    if (ph.kind == kPhaseNear)
-      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) is_near[t] = split ? 1 : 0;
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+        if (f >= 1.0 || sel[plan.tasks[t].node]) {
+          want[t] = 1;
+          if (ph.kind == kPhaseNear) is_near[t] = 1;
+        }
   std::vector<std::uint8_t> seen_sub(plan.tasks.size() * std::size_t(ncb) * S, 0);
   for (std::uint64_t it : items) {
     const std::uint32_t t = static_cast<std::uint32_t>(it), cb = item_cb(it), sub = item_sub(it);
@@ -1888,7 +1931,8 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   for (std::size_t i = 0; i < nn; ++i) {
     if (wr[i] && wr[i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: T target != writer tiles");
     if (wr[nn + i] && wr[nn + i] != plan.node_tiles[i]) return set_err(HMXG_EINVAL, "dag: S target != writer tiles");
-    if (split && wr[2 * nn + i] != plan.yp_tiles[i]) return set_err(HMXG_EINVAL, "dag: Yp target != near tiles");
+    if (split && (f >= 1.0 || sel[i]) && wr[2 * nn + i] != plan.yp_tiles[i])
+      return set_err(HMXG_EINVAL, "dag: Yp target != near tiles");
   }
   // (2) topological: every tile an item waits for is complete before it in the claim order
   std::vector<std::uint32_t> done(3 * nn * std::size_t(ncb), 0);

@@ -308,3 +308,20 @@ def test_dag_check_ctree_mode(monkeypatch):
             assert N.hmxg().hmxg_dag_check(C.byref(v), q, 444, C.byref(n_ct)) == 0, N.last_error(N.hmxg(), "hmxg")
             assert 0 < n_ct.value < n_dag.value  # the near tiles only
         inst.close()
+
+
+@pytest.mark.parametrize("frac", ["0.1", "0.35", "1"])
+def test_dag_check_partial_split(frac, monkeypatch):
+    """A partial split (HMXG_SPLIT_FRAC): a fraction of the leaves run as split-variant near
+    tiles between the tree levels plus accumulating tiles at the end, the rest as combined
+    tiles; the claim order stays topological and every tile appears once per column block."""
+    from paper_1812_07152_b200 import config
+
+    monkeypatch.setenv("HMXG_SPLIT_FRAC", frac)
+    insts = [build_instance(config("cfg1-hss")[0]), _small(),
+             build_instance(InstanceSpec(n=3000, d=3, leaf=48, max_rank=40, mode="budget", budget=0.1, seed=12))]
+    for inst in insts:
+        v = inst.cds.view()
+        for q, grid in [(2048, 444), (640, 444), (64, 2)]:
+            assert N.hmxg().hmxg_dag_check(C.byref(v), q, grid, None) == 0, N.last_error(N.hmxg(), "hmxg")
+        inst.close()

@@ -14,7 +14,6 @@ timeout 900 python bench.py --impl reference > gpurun_out/${T}_reference.json 2>
 for c in cfg1-hss cfg2-h2b cfg3-h2b cfg4-h2b; do
   timeout 900 python bench.py --config $c --dropin-steps 1 > gpurun_out/${T}_bench_$c.json 2> gpurun_out/${T}_bench_$c.err
 done
-SHORT="--steps 2 --warmup 1 --extra '' --e2e-steps 0 --dropin-steps 0 --no-cpu-baseline"
 timeout 600 python bench.py --steps 2 --warmup 1 --extra "" --e2e-steps 0 --dropin-steps 0 --no-cpu-baseline > gpurun_out/${T}_plain.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches_cfg5.csv \
     python bench.py --steps 2 --warmup 1 --extra "" --e2e-steps 0 --dropin-steps 0 --no-cpu-baseline > gpurun_out/${T}_ncu_launches.log 2>&1
