@@ -75,6 +75,7 @@ def _ref_lib():
             "hmxr_samples": (C.c_int, [vp, vp, vp]),
             "hmxr_basis": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(u64), vp, vp]),
             "hmxr_compress_seconds": (C.c_double, [vp]),
+            "hmxr_bases_seconds": (C.c_double, [vp, C.POINTER(C.c_uint64)]),
             "hmxr_generate_plan": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_uint32)]),
             "hmxr_mix64": (u64, [u64]),
             "hmxr_rng_fill_pm1": (None, [u64, u64, vp]),

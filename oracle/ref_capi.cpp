@@ -449,6 +449,44 @@ int hmxr_basis(void* inst, std::uint32_t node, std::uint32_t* srank, std::uint64
 
 double hmxr_compress_seconds(void* inst) { return static_cast<RefInstance*>(inst)->compress_seconds; }
 
+// The bases part of hmx::compress alone (compress.cpp:113-146: per participating node,
+// deepest level first, the sampled block through hmx::dense_block and the reference's
+// interpolative_decomposition), timed on one host thread: the like-for-like CPU figure for
+// the GPU's hmxg_compress, which computes the bases only. Returns seconds (< 0: failure);
+// *rank_sum gets the sum of the sranks (the same as the instance's bases).
+double hmxr_bases_seconds(void* inst, std::uint64_t* rank_sum) {
+  auto* in = static_cast<RefInstance*>(inst);
+  double secs = -1.0;
+  guarded([&] {
+    const auto& tree = in->ht.tree;
+    std::vector<std::vector<hmx::index_t>> by_level(tree.height + 1);
+    for (hmx::index_t i = 0; i < tree.num_nodes; ++i)
+      if (in->cm.participating[i]) by_level[tree.level[i]].push_back(i);
+    std::vector<std::vector<hmx::index_t>> skel(tree.num_nodes);
+    std::uint64_t rs = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (auto lvl = by_level.size(); lvl-- > 0;)
+      for (hmx::index_t node : by_level[lvl]) {
+        std::vector<hmx::index_t> cols;
+        if (tree.is_leaf(node)) {
+          const auto members = tree.node_points(node);
+          cols.assign(members.begin(), members.end());
+        } else {
+          cols = skel[tree.lchild[node]];
+          cols.insert(cols.end(), skel[tree.rchild[node]].begin(), skel[tree.rchild[node]].end());
+        }
+        if (cols.empty()) continue;
+        const hmx::DenseMatrix block = hmx::dense_block(in->kernel, in->pts, in->si.rows[node], cols);
+        const hmx::IdResult id = hmx::interpolative_decomposition(block, in->cm.bacc, in->cm.max_rank);
+        for (hmx::index_t local : id.skeleton) skel[node].push_back(cols[local]);
+        rs += id.srank;
+      }
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rank_sum) *rank_sum = rs;
+  });
+  return secs;
+}
+
 // hmx::generate_plan (executor.cpp:259-272) over the instance's own tree, blocks and
 // coarsening with p workers: the stock plan, as lowering bits for hmxr_evaluate.
 int hmxr_generate_plan(void* inst, std::uint32_t p, std::uint32_t* bits) {
