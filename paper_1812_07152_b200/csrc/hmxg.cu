@@ -838,8 +838,8 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       const DevState::Wave& wv = d.waves[w];
       const std::uint64_t nch = wv.c1 - wv.c0;
       if (nch) {
-        gen_near<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 148ull * 16)), 256, 0, st>>>(
-            d.pts, d.kp, d.pmap, d.gen_chunks + wv.c0, nch, d.tiles);
+        gen_near<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 148ull * 8)), 256, 80 * d.kp.d * sizeof(double),
+                   st>>>(d.pts, d.kp, d.pmap, d.gen_chunks + wv.c0, nch, d.tiles);
         ++*launches;
         desc(7, static_cast<std::uint32_t>(w), static_cast<std::uint32_t>(nch), 0.0, 8.0 * kChunkElems * nch, 0.0);
         HMXG_TRY(mark());
@@ -1456,6 +1456,9 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       HMXG_CUDA(cudaGetLastError());
     }
     if (otf) {  // the points and every wave's near chunks; the near blocks themselves never exist
+      const std::size_t gsm = 80 * std::size_t(near_src->d) * sizeof(double);
+      if (gsm > 200 * 1024) return set_err(HMXG_EINVAL, "hmxg_upload: near field on the fly supports d <= 320");
+      HMXG_CUDA(cudaFuncSetAttribute(gen_near, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsm)));
       HMXG_TRY(dev_upload(&d.pts, near_src->coords, cds->n * near_src->d, d.comp));
       HMXG_TRY(dev_upload(&d.gen_chunks, otf_l.chunks.data(), otf_l.chunks.size(), d.comp));
       d.kp = near_src->kp;

@@ -234,23 +234,44 @@ struct GenChunk {
 static_assert(sizeof(GenChunk) == 24, "GenChunk layout");
 
 // A wave's near-field chunks into the scratch region of the tiles (one launch per wave, before
-// the wave's leaf rows): consecutive threads write consecutive (swizzled) rows of a chunk.
+// the wave's leaf rows). Per chunk the CTA stages its 64 row points' and 16 column points'
+// coordinates in shared memory (dim-major, so consecutive threads read consecutive rows),
+// then every thread forms 4 entries with kernel_value's exact operation sequence and writes
+// them swizzled. Dynamic shared memory: 80 * d doubles.
 __global__ void __launch_bounds__(256) gen_near(const double* __restrict__ pts, const KernelParams kp,
                                                 const std::uint32_t* __restrict__ pmap,
                                                 const GenChunk* __restrict__ chunks, std::uint64_t nchunks,
                                                 double* __restrict__ tiles) {
+  extern __shared__ double xs[];  // [d][80]: rows 0..63 then columns 64..79
+  const std::uint32_t d = kp.d;
   for (std::uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const GenChunk g = chunks[c];
+    for (std::uint32_t e = threadIdx.x; e < 80u * d; e += blockDim.x) {
+      const std::uint32_t p = e / d, i = e % d;  // point slot, dimension
+      double v = 0.0;
+      if (p < 64 ? p < g.m : p - 64 < g.kvalid) {
+        const std::uint64_t pt = __ldg(pmap + (p < 64 ? g.yrow + p : g.brow + (p - 64)));
+        v = __ldg(pts + pt * d + i);
+      }
+      xs[i * 80 + p] = v;
+    }
+    __syncthreads();
     double* out = tiles + g.out * 1024u;
-    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
-      const int r = e & 63, k = e >> 6;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * 256, r = e & 63, k = e >> 6;
       double v = 0.0;
       if (r < g.m && k < g.kvalid) {
-        const std::uint64_t pi = __ldg(pmap + g.yrow + r), pj = __ldg(pmap + g.brow + k);
-        v = kernel_value(kp, pts + pi * kp.d, pts + pj * kp.d);
+        double s = 0.0;
+        for (std::uint32_t i = 0; i < d; ++i) {
+          const double t = __dsub_rn(xs[i * 80 + r], xs[i * 80 + 64 + k]);
+          s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        v = kernel_of_sqdist(kp, s);
       }
       out[k * 64 + (r ^ ((k & 3) << 2))] = v;  // a_swz(k, r)
     }
+    __syncthreads();
   }
 }
 
