@@ -27,18 +27,29 @@ class NodeBasis:
     v: np.ndarray
 
 
+_CONTEXTS: dict = {}
+
+
+def _context(device: int):
+    """One evaluator context per device for the process (creating one per call costs more
+    than a small compression)."""
+    from .executor import Context
+
+    if device not in _CONTEXTS:
+        _CONTEXTS[device] = Context((device,))
+    return _CONTEXTS[device]
+
+
 def gpu_compress(points: np.ndarray, kernel: Kernel, cds: CDS, sample_ptr: np.ndarray, sample_idx: np.ndarray,
                  bacc: float, max_rank: int, device: int = 0) -> list[NodeBasis]:
     """Bases of every node of ``cds``'s tree (participation from ``cds.participating``);
     ``sample_ptr``/``sample_idx`` are hmx::SampleInfo::rows in CSR form."""
-    from .executor import Context
-
     pts = np.ascontiguousarray(points, dtype=np.float64)
     sp = np.ascontiguousarray(sample_ptr, dtype=np.uint64)
     si = np.ascontiguousarray(sample_idx, dtype=np.uint32)
     if sp.size != cds.num_nodes + 1:
         raise ValueError("compress: sampling info does not match tree")
-    ctx = Context((device,))
+    ctx = _context(device)
     lib = N.hmxg()
     h = C.c_void_p()
 
@@ -72,7 +83,6 @@ def gpu_compress(points: np.ndarray, kernel: Kernel, cds: CDS, sample_ptr: np.nd
     finally:
         if h:
             lib.hmxg_compressed_free(h)
-        ctx.close()
 
 
 def skeleton_csr(bases: list[NodeBasis]) -> tuple[np.ndarray, np.ndarray]:

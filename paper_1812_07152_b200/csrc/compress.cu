@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -36,6 +38,7 @@ namespace {
 
 constexpr unsigned kIdThreads = 256;
 constexpr double kRankFloor = 1e-14;  // compress.cpp:13
+constexpr int kChain = 16;            // column-chain loads per block (two blocks in flight)
 
 // One node's decomposition.
 struct IdJob {
@@ -75,6 +78,36 @@ __device__ __forceinline__ void block_reduce_max_sum(double& best, std::uint32_t
   __syncthreads();
 }
 
+// s (+)= f(x_i) over rows [k, r) of one column (stride c), in row order (the reference's
+// sum), with the next kChain rows' loads in flight while the current block is added: the
+// chain is bound by the add latency, not by an L2 round trip per block.
+template <class F>
+__device__ __forceinline__ double chain_sum(const double* __restrict__ col, std::uint32_t c, std::uint32_t k,
+                                            std::uint32_t r, F&& f) {
+  double s = 0.0;
+  std::uint32_t i = k;
+  if (i + kChain <= r) {
+    double x0[kChain], x1[kChain];
+#pragma unroll
+    for (int u = 0; u < kChain; ++u) x0[u] = col[static_cast<std::uint64_t>(i + u) * c];
+    for (;;) {
+      const bool more = i + 2 * kChain <= r;
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < kChain; ++u) x1[u] = col[static_cast<std::uint64_t>(i + kChain + u) * c];
+      }
+#pragma unroll
+      for (int u = 0; u < kChain; ++u) s = __dadd_rn(s, f(i + u, x0[u]));
+      i += kChain;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < kChain; ++u) x0[u] = x1[u];
+    }
+  }
+  for (; i < r; ++i) s = __dadd_rn(s, f(i, col[static_cast<std::uint64_t>(i) * c]));
+  return s;
+}
+
 __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict__ pts, const KernelParams kp,
                                                       const IdJob* __restrict__ jobs,
                                                       const std::uint32_t* __restrict__ samp,
@@ -86,12 +119,13 @@ __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict_
   const IdJob job = jobs[blockIdx.x];
   const std::uint32_t r = job.r, c = job.c, cap = job.cap;
   double* a = scratch + job.a_off;
-  double* v = scratch + job.v_off;
+  (void)job.v_off;  // (the Householder vector lives in shared memory)
   std::uint32_t* piv = piv_out + job.piv_off;
   double* norms2 = reinterpret_cast<double*>(smem);               // c
   double* red_val = norms2 + c;                                   // blockDim
   double* red_sum = red_val + blockDim.x;                         // blockDim
-  std::uint32_t* red_idx = reinterpret_cast<std::uint32_t*>(red_sum + blockDim.x);  // blockDim
+  double* vs = red_sum + blockDim.x;                              // r: the Householder vector
+  std::uint32_t* red_idx = reinterpret_cast<std::uint32_t*>(vs + r);  // blockDim
   __shared__ double s_v2, s_xnorm;
   const unsigned t = threadIdx.x, nt = blockDim.x;
 
@@ -122,11 +156,9 @@ __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict_
     double best = -1.0, rem = 0.0;
     std::uint32_t best_j = 0xffffffffu;
     for (std::uint32_t j = k + t; j < c; j += nt) {
-      double s = 0.0;
-      for (std::uint32_t i = k; i < r; ++i) {
-        const double x = a[static_cast<std::uint64_t>(i) * c + j];
-        s = __dadd_rn(s, __dmul_rn(x, x));
-      }
+      // rows in order (the reference's sum), loads issued kChain ahead of the adds: the
+      // chain is bound by the add latency, not by one L2 round trip per row
+      const double s = chain_sum(a + j, c, k, r, [](std::uint32_t, double x) { return __dmul_rn(x, x); });
       norms2[j] = s;
       rem += s;
       if (s > best) {  // strictly greater: the first maximum of this thread's columns
@@ -152,18 +184,18 @@ __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict_
     }
     __syncthreads();
     // Householder reflector zeroing column k below the diagonal (compress.cpp:55-76)
-    for (std::uint32_t i = k + 1 + t; i < r; i += nt) v[i - k] = a[static_cast<std::uint64_t>(i) * c + k];
+    for (std::uint32_t i = k + 1 + t; i < r; i += nt) vs[i - k] = a[static_cast<std::uint64_t>(i) * c + k];
     if (t == 0) {
       const double ckk = a[static_cast<std::uint64_t>(k) * c + k];
       double xnorm = __dsqrt_rn(norms2[pivot]);
       if (ckk > 0) xnorm = -xnorm;
-      v[0] = __dsub_rn(ckk, xnorm);
+      vs[0] = __dsub_rn(ckk, xnorm);
       s_xnorm = xnorm;
     }
     __syncthreads();
     if (t == 0) {
       double v2 = 0.0;
-      for (std::uint32_t i = 0; i < r - k; ++i) v2 = __dadd_rn(v2, __dmul_rn(v[i], v[i]));
+      for (std::uint32_t i = 0; i < r - k; ++i) v2 = __dadd_rn(v2, __dmul_rn(vs[i], vs[i]));
       s_v2 = v2;
       a[static_cast<std::uint64_t>(k) * c + k] = s_xnorm;
     }
@@ -172,13 +204,13 @@ __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict_
     const double v2 = s_v2;
     if (v2 > 0.0) {
       for (std::uint32_t j = k + 1 + t; j < c; j += nt) {
-        double dot = 0.0;
-        for (std::uint32_t i = k; i < r; ++i)
-          dot = __dadd_rn(dot, __dmul_rn(v[i - k], a[static_cast<std::uint64_t>(i) * c + j]));
+        double* col = a + j;
+        const double dot = chain_sum(col, c, k, r, [&](std::uint32_t i, double x) { return __dmul_rn(vs[i - k], x); });
         const double f = __ddiv_rn(__dmul_rn(2.0, dot), v2);
-        for (std::uint32_t i = k; i < r; ++i) {
-          double* x = a + static_cast<std::uint64_t>(i) * c + j;
-          *x = __dsub_rn(*x, __dmul_rn(f, v[i - k]));
+#pragma unroll 16
+        for (std::uint32_t i2 = k; i2 < r; ++i2) {
+          double* x = col + static_cast<std::uint64_t>(i2) * c;
+          *x = __dsub_rn(*x, __dmul_rn(f, vs[i2 - k]));
         }
       }
     }
@@ -304,11 +336,26 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
   std::uint32_t*& d_piv = lb.piv;
   std::uint32_t*& d_rank = lb.rank;
   std::size_t cap_jobs = 0, cap_cols = 0, cap_scratch = 0, cap_vout = 0, cap_piv = 0, cap_rank = 0;
+  // per level: its device V buffer and where every node's V sits in it
+  struct LevelV {
+    double* vout = nullptr;
+    std::uint64_t elems = 0;
+    struct Part {
+      std::uint32_t node;
+      std::uint64_t off, count;
+    };
+    std::vector<Part> parts;
+    LevelV() = default;
+    LevelV(LevelV&& o) noexcept : vout(o.vout), elems(o.elems), parts(std::move(o.parts)) { o.vout = nullptr; }
+    LevelV(const LevelV&) = delete;
+    ~LevelV() { cudaFree(vout); }
+  };
+  std::vector<LevelV> levels_v;
   for (std::uint32_t lvl = height + 1; lvl-- > 0;) {  // deepest level first (compress.cpp:117-121)
     std::vector<IdJob> jobs;
     std::vector<std::uint32_t> job_node, colbuf;
     std::uint64_t scratch = 0, vsize = 0, pivsize = 0;
-    std::uint32_t max_c = 0;
+    std::uint32_t max_c = 0, max_r = 0;
     for (std::uint32_t node : by_level[lvl]) {
       const std::uint64_t r = sample_ptr[node + 1] - sample_ptr[node];
       std::vector<std::uint32_t> cl;
@@ -340,6 +387,7 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
       j.piv_off = pivsize;
       pivsize += j.c;
       max_c = std::max(max_c, j.c);
+      max_r = std::max(max_r, j.r);
       jobs.push_back(j);
       job_node.push_back(node);
       skel[node] = std::move(cl);  // the node's columns; replaced by its skeleton below
@@ -353,18 +401,40 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
     HMXG_TRY(grow(&d_rank, cap_rank, jobs.size()));
     HMXG_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(IdJob), cudaMemcpyHostToDevice, st));
     HMXG_CUDA(cudaMemcpyAsync(d_cols, colbuf.data(), colbuf.size() * 4, cudaMemcpyHostToDevice, st));
-    const std::size_t smem = max_c * sizeof(double) + kIdThreads * (2 * sizeof(double) + sizeof(std::uint32_t));
+    const std::size_t smem =
+        (max_c + max_r) * sizeof(double) + kIdThreads * (2 * sizeof(double) + sizeof(std::uint32_t));
     if (smem > 200 * 1024) return set_err(HMXG_EINVAL, "hmxg_compress: too many columns in one block");
     if (smem > 48 * 1024) HMXG_CUDA(cudaFuncSetAttribute(id_level, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    const bool trace = std::getenv("HMXG_COMPRESS_TRACE") != nullptr;
+    if (trace) {
+      cudaEventCreate(&te0);
+      cudaEventCreate(&te1);
+      cudaEventRecord(te0, st);
+    }
     id_level<<<static_cast<unsigned>(jobs.size()), kIdThreads, smem, st>>>(d_pts, kp, d_jobs, d_samp, d_cols, bacc,
                                                                           d_scratch, d_vout, d_piv, d_rank);
+    if (trace) {
+      cudaEventRecord(te1, st);
+      cudaEventSynchronize(te1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, te0, te1);
+      std::fprintf(stderr, "[hmxg_compress] level %u: %zu nodes, max r %u, max c %u, kernel %.3f ms\n", lvl,
+                   jobs.size(), max_r, max_c, ms);
+      cudaEventDestroy(te0);
+      cudaEventDestroy(te1);
+    }
     HMXG_CUDA(cudaGetLastError());
+    // only the ranks and pivots come back per level (the next level's columns are the
+    // skeletons); the bases stay on the device until the end
     std::vector<std::uint32_t> ranks(jobs.size()), piv(pivsize);
-    std::vector<double> vh(vsize);
     HMXG_CUDA(cudaMemcpyAsync(ranks.data(), d_rank, ranks.size() * 4, cudaMemcpyDeviceToHost, st));
     HMXG_CUDA(cudaMemcpyAsync(piv.data(), d_piv, piv.size() * 4, cudaMemcpyDeviceToHost, st));
-    HMXG_CUDA(cudaMemcpyAsync(vh.data(), d_vout, vh.size() * 8, cudaMemcpyDeviceToHost, st));
     HMXG_CUDA(cudaStreamSynchronize(st));
+    LevelV lv;
+    lv.vout = d_vout;  // this level's V buffer is kept; the next level allocates its own
+    d_vout = nullptr;
+    cap_vout = 0;
     for (std::size_t q = 0; q < jobs.size(); ++q) {
       const std::uint32_t node = job_node[q], k = ranks[q], c = jobs[q].c;
       const std::vector<std::uint32_t> cl = std::move(skel[node]);
@@ -373,7 +443,21 @@ int hmxg_compress(hmxg_ctx* ctx, const double* coords, uint64_t n, uint32_t d, i
       skel[node] = std::move(sk);
       res->srank[node] = k;
       vrows[node] = c;
-      vmat[node].assign(vh.begin() + jobs[q].out_off, vh.begin() + jobs[q].out_off + std::uint64_t(c) * k);
+      lv.parts.push_back({node, jobs[q].out_off, std::uint64_t(c) * k});
+    }
+    lv.elems = vsize;
+    levels_v.push_back(std::move(lv));
+  }
+  // every level's bases, read back once at the end
+  {
+    std::uint64_t most = 0;
+    for (const LevelV& lv : levels_v) most = std::max(most, lv.elems);
+    std::vector<double> vh(most);
+    for (const LevelV& lv : levels_v) {
+      if (!lv.elems) continue;
+      HMXG_CUDA(cudaMemcpyAsync(vh.data(), lv.vout, lv.elems * sizeof(double), cudaMemcpyDeviceToHost, st));
+      HMXG_CUDA(cudaStreamSynchronize(st));
+      for (const auto& pt : lv.parts) vmat[pt.node].assign(vh.begin() + pt.off, vh.begin() + pt.off + pt.count);
     }
   }
   // flatten
