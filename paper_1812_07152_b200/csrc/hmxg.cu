@@ -679,7 +679,8 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
   for (const Phase& ph : plan.split_phases) phs.push_back(&ph);
   FILE* f = std::fopen(path, "w");
   if (!f) return;
-  std::fprintf(f, "cta,seq,sm,item,task,cb,kind,level,m,segs,chunks,t_claim,t_issued,t_take,t_kend,t_done,t_first,t_deps\n");
+  std::fprintf(f, "cta,seq,sm,item,task,cb,kind,level,m,segs,chunks,t_claim,t_issued,t_take,t_kend,t_done,t_first,t_deps,"
+               "node,sub\n");
   for (std::size_t b = 0; b < g_trace_words / (kTraceSeq * kTraceWords); ++b)
     for (int s = 0; s < kTraceSeq; ++s) {
       const unsigned long long* r = &h[(b * kTraceSeq + s) * kTraceWords];
@@ -697,9 +698,9 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
       const Task& tk = plan.tasks[task];
       unsigned chunks = 0;
       for (std::uint32_t sgi = tk.seg_begin; sgi < tk.seg_end; ++sgi) chunks += plan.segs[sgi].nchunks;
-      std::fprintf(f, "%zu,%d,%llu,%u,%u,%u,%d,%d,%u,%u,%u,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", b, s, r[0] >> 32, qi,
-                   task, cb, kind, level, tk.m, tk.seg_end - tk.seg_begin, chunks, r[1], r[2], r[3], r[4], r[5], r[6],
-                   r[7]);
+      std::fprintf(f, "%zu,%d,%llu,%u,%u,%u,%d,%d,%u,%u,%u,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%u,%u\n", b, s, r[0] >> 32,
+                   qi, task, cb, kind, level, tk.m, tk.seg_end - tk.seg_begin, chunks, r[1], r[2], r[3], r[4], r[5], r[6],
+                   r[7], tk.node, item_sub(items[qi]));
     }
   std::fclose(f);
   // CTree clusters: per CTA start, tables copied, end of each level

@@ -893,6 +893,12 @@ __device__ __forceinline__ unsigned long long* trace_slot(const D& d, std::uint3
   } while (0)
 #endif
 
+#ifndef HMXG_SPIN_MAX_NS
+#define HMXG_SPIN_MAX_NS 256
+#endif
+#ifndef HMXG_SPIN_SVC_MAX_NS
+#define HMXG_SPIN_SVC_MAX_NS 128
+#endif
 __device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
   std::uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -904,7 +910,7 @@ __device__ __forceinline__ void spin_until(const std::uint32_t* p, std::uint32_t
   std::uint32_t polls = 0;
   while (ld_acquire(p) < target) {
     __nanosleep(ns);
-    ns = min(ns * 2, 256u);
+    ns = min(ns * 2, static_cast<unsigned>(HMXG_SPIN_MAX_NS));
     if (++polls > (1u << 24)) __trap();  // ~4 s: a missing dependency signal, not a slow tile
   }
 }
@@ -918,7 +924,7 @@ __device__ __forceinline__ void spin_until_svc(const std::uint32_t* p, std::uint
   while (ld_acquire(p) < target) {
     svc();
     __nanosleep(ns);
-    ns = min(ns * 2, 128u);
+    ns = min(ns * 2, static_cast<unsigned>(HMXG_SPIN_SVC_MAX_NS));
     if (++polls > (1u << 25)) __trap();
   }
 }
