@@ -561,7 +561,8 @@ def ours(args) -> None:
     # the heavier half of the headline config (BASELINE cfg5 names HSS and H2-b): same
     # measurement, same rank layout, reported under extra
     extra = {}
-    if args.extra and args.config == "cfg5-hss":
+    # (one GPU only: every rank would build cfg5-H2-b's 18.6 GB near field on the host)
+    if args.extra and args.config == "cfg5-hss" and world == 1:
         for xname in args.extra.split(","):
             x = measure(args, xname, env, args.steps, args.warmup, min(args.e2e_steps, 2), min(args.dropin_steps, 1))
             extra[xname.replace("-", "_")] = {
@@ -571,7 +572,7 @@ def ours(args) -> None:
                 "gpu_launches": x["launches"], "clocks": x["clk"], "phases_ms": x["phases_ms"], "cds": x["cds_info"],
                 "cds_gb": x["cds_gb"]}
 
-    if args.extra and args.config == "cfg5-hss" and args.near_otf:
+    if args.extra and args.config == "cfg5-hss" and args.near_otf and world == 1:
         extra["cfg5_h2b_near_on_the_fly"] = measure_near_otf(args, "cfg5-h2b", env, max(3, args.steps // 2), args.warmup)
 
     clk_all = [m["clk"]]
