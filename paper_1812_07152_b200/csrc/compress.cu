@@ -193,10 +193,8 @@ __global__ void __launch_bounds__(kIdThreads) id_level(const double* __restrict_
       s_xnorm = xnorm;
     }
     __syncthreads();
-    if (t == 0) {
-      double v2 = 0.0;
-      for (std::uint32_t i = 0; i < r - k; ++i) v2 = __dadd_rn(v2, __dmul_rn(vs[i], vs[i]));
-      s_v2 = v2;
+    if (t == 0) {  // ||v||^2 in order; the shared-memory loads run kChain ahead of the adds
+      s_v2 = chain_sum(vs, 1, 0, r - k, [](std::uint32_t, double x) { return __dmul_rn(x, x); });
       a[static_cast<std::uint64_t>(k) * c + k] = s_xnorm;
     }
     for (std::uint32_t i = k + 1 + t; i < r; i += nt) a[static_cast<std::uint64_t>(i) * c + k] = 0.0;
