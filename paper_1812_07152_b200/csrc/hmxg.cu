@@ -324,6 +324,23 @@ int ensure_stage(const Plan& plan, DevState& d, std::size_t q) {
 #ifndef HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA
 #define HMXG_SPLIT_LEAF_MAX_ITEMS_PER_CTA 48
 #endif
+// The plan options of a replicated upload (HMXG_NO_FLAT=1: no flat tree, see Plan::flat_phases).
+SplitSpec plan_spec() {
+  SplitSpec s;
+  s.flat_tree = std::getenv("HMXG_NO_FLAT") == nullptr;
+  return s;
+}
+// The tree phases an evaluation runs, in order: the upward and far+downward phases, or, for a
+// flat tree (Plan::flat_phases, small trees), the leaf upward phase and the two flat phases.
+std::vector<const Phase*> tree_phases(const Plan& plan, std::uint32_t stage) {
+  std::vector<const Phase*> out;
+  for (const Phase& ph : plan.phases)
+    if (ph.stage == stage && ph.kind != kPhaseLeaf && (!plan.flat || (ph.kind == kPhaseUp && ph.level == 0)))
+      out.push_back(&ph);
+  if (plan.flat && stage == 0)
+    for (const Phase& ph : plan.flat_phases) out.push_back(&ph);
+  return out;
+}
 std::uint32_t ctree_csize(const Plan& plan, std::size_t q, unsigned grid);
 bool split_leaf(const Plan& plan, std::size_t q, unsigned grid) {
   if (plan.split_phases.empty() || plan.near_otf) return false;  // on-the-fly near field: combined tasks
@@ -335,10 +352,11 @@ bool split_leaf(const Plan& plan, std::size_t q, unsigned grid) {
 // The level-by-level launch sequence for q columns (HMXG_F_LEVEL_LAUNCHES): the same leaf
 // variant as the DAG launch, so both give the same bits.
 std::vector<const Phase*> level_phases(const Plan& plan, std::size_t q, unsigned grid) {
-  std::vector<const Phase*> out;
+  std::vector<const Phase*> out = tree_phases(plan, 0);
   const bool split = split_leaf(plan, q, grid);
-  for (const Phase& ph : plan.phases)
-    if (!(split && ph.kind == kPhaseLeaf)) out.push_back(&ph);
+  if (!split)
+    for (const Phase& ph : plan.phases)
+      if (ph.kind == kPhaseLeaf) out.push_back(&ph);
   if (split)
     for (const Phase& ph : plan.split_phases) out.push_back(&ph);
   return out;
@@ -410,13 +428,11 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
   // tree phases; the leaf rows: combined tasks of the leaves not split, the near tasks and the
   // accumulating tasks of the split ones (and every near task when f = 1: those of leaves
   // without a basis are their final rows)
-  std::vector<const Phase*> tree;
+  const std::vector<const Phase*> tree = tree_phases(plan, stage);
   std::vector<std::uint32_t> near, tail;
   for (const Phase& ph : plan.phases) {
     if (ph.stage != stage) continue;
-    if (ph.kind != kPhaseLeaf) {
-      tree.push_back(&ph);
-    } else if (f < 1.0 && !plan.near_otf) {  // on the fly: the leaf rows run in waves
+    if (ph.kind == kPhaseLeaf && f < 1.0 && !plan.near_otf) {  // on the fly: the leaf rows run in waves
       for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
         if (!sel[plan.tasks[t].node]) tail.push_back(t);
     }
@@ -525,7 +541,7 @@ double ct_dmma_per_octet(const Plan& plan) {
   return tasks ? n : 1e300;  // no tree tasks: nothing for a CTree
 }
 std::uint32_t ctree_csize(const Plan& plan, std::size_t q, unsigned grid) {
-  if (!fused_io(plan, q) || plan.split_phases.empty() || !std::getenv("HMXG_CTREE")) return 0;
+  if (!fused_io(plan, q) || plan.split_phases.empty() || plan.flat || !std::getenv("HMXG_CTREE")) return 0;
   if (plan.ct_dmma < 0.0) plan.ct_dmma = ct_dmma_per_octet(plan);
   if (plan.ct_dmma > HMXG_CT_MAX_DMMA_PER_OCTET || plan.ct_smem > std::uint64_t(kStages) * kStageBytes) return 0;
   const std::size_t noct = (q + 7) / 8;
@@ -677,6 +693,7 @@ void trace_dump(const Plan& plan, std::size_t q, unsigned grid) {
   std::vector<const Phase*> phs;
   for (const Phase& ph : plan.phases) phs.push_back(&ph);
   for (const Phase& ph : plan.split_phases) phs.push_back(&ph);
+  for (const Phase& ph : plan.flat_phases) phs.push_back(&ph);
   FILE* f = std::fopen(path, "w");
   if (!f) return;
   std::fprintf(f, "cta,seq,sm,item,task,cb,kind,level,m,segs,chunks,t_claim,t_issued,t_take,t_kend,t_done,t_first,t_deps,"
@@ -1386,7 +1403,9 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
   auto mat = std::make_unique<hmxg_mat>();
   mat->ctx = ctx;
   std::string err;
-  if (!build_plan(*cds, kBM, mat->plan, err, split)) return set_err(HMXG_EINVAL, err);
+  SplitSpec spec = split;
+  spec.flat_tree = spec.flat_tree && std::getenv("HMXG_NO_FLAT") == nullptr;
+  if (!build_plan(*cds, kBM, mat->plan, err, spec)) return set_err(HMXG_EINVAL, err);
   OtfLayout otf_l;
   if (otf) {
     if (!near_src || split.nparts != 1) return set_err(HMXG_EINVAL, "hmxg_upload: near field on the fly needs points");
@@ -1441,6 +1460,8 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       HMXG_TRY(dev_upload(&gd, gsrc[kGenD], plan.d_elems, d.comp));
     if (!near_src || !near_src->skel_ptr) HMXG_TRY(dev_upload(&gb, gsrc[kGenB], plan.b_elems, d.comp));
     HMXG_TRY(dev_upload(&gv, gsrc[kGenV], plan.v_elems, d.comp));
+    double* gc = nullptr;  // the flat tree's composite blocks (Plan::cgen)
+    HMXG_TRY(dev_upload(&gc, plan.cgen.data(), plan.cgen.size(), d.comp));
     const std::vector<TileSrc>& tsrc = otf ? otf_l.srcs : plan.tile_src;
     const std::vector<std::uint32_t>& tcseg = otf ? otf_l.cseg : plan.chunk_seg;
     const std::uint64_t tile_elems = otf ? otf_l.resident_elems + otf_l.scratch_elems : plan.tile_elems;
@@ -1452,8 +1473,8 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       HMXG_CUDA(cudaMalloc(&d.tiles, tile_elems * sizeof(double)));
       const std::uint64_t nch = tcseg.size();
       if (nch)
-        tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, srcs, cseg,
-                                                                                                 maps, d.tiles, nch);
+        tile_a<<<static_cast<unsigned>(std::min<std::uint64_t>(nch, 1u << 20)), 256, 0, d.comp>>>(gd, gb, gv, gc, srcs,
+                                                                                                 cseg, maps, d.tiles, nch);
       HMXG_CUDA(cudaGetLastError());
     }
     if (otf) {  // the points and every wave's near chunks; the near blocks themselves never exist
@@ -1471,6 +1492,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     cudaFree(gd);
     cudaFree(gb);
     cudaFree(gv);
+    cudaFree(gc);
     cudaFree(srcs);
     cudaFree(cseg);
     cudaFree(maps);
@@ -1791,7 +1813,7 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
   if (!cds) return set_err(HMXG_EINVAL, "hmxg_validate: null view");
   Plan plan;
   std::string err;
-  if (!build_plan(*cds, kBM, plan, err)) return set_err(HMXG_EINVAL, err);
+  if (!build_plan(*cds, kBM, plan, err, plan_spec())) return set_err(HMXG_EINVAL, err);
   if (info) {
     std::memset(info, 0, sizeof *info);
     info->n = plan.n;
@@ -1801,7 +1823,9 @@ int hmxg_validate(const hmxg_cds_view* cds, hmxg_info* info) {
     info->skel_rows = plan.skel_rows;
     info->launches_per_eval = 3;
     info->flops_per_col = 2.0 * (2.0 * plan.v_elems + plan.b_elems + plan.d_elems);
-    for (const Phase& ph : plan.phases) info->exec_flops_per_col += ph.flops_per_col;
+    for (const Phase* ph : tree_phases(plan, 0)) info->exec_flops_per_col += ph->flops_per_col;
+    for (const Phase& ph : plan.phases)
+      if (ph.kind == kPhaseLeaf) info->exec_flops_per_col += ph.flops_per_col;
   }
   return HMXG_OK;
 }
@@ -1887,7 +1911,7 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   if (!cds || q == 0 || grid == 0) return set_err(HMXG_EINVAL, "hmxg_dag_check: null view, q = 0 or grid = 0");
   Plan plan;
   std::string err;
-  if (!build_plan(*cds, kBM, plan, err)) return set_err(HMXG_EINVAL, err);
+  if (!build_plan(*cds, kBM, plan, err, plan_spec())) return set_err(HMXG_EINVAL, err);
   const std::uint32_t ncb = static_cast<std::uint32_t>((q + kBN - 1) / kBN);
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
   if (nitems) *nitems = items.size();
@@ -1901,9 +1925,12 @@ int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* 
   // ones (every near task when f = 1)
   std::vector<std::uint32_t> want(plan.tasks.size(), 0), seen(plan.tasks.size() * std::size_t(ncb), 0);
   std::vector<std::uint8_t> is_near(plan.tasks.size(), 0);
+  for (const Phase* ph : tree_phases(plan, 0))
+    for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) want[t] = 1;
   for (const Phase& ph : plan.phases)
-    for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
-      if (ph.kind != kPhaseLeaf || (f < 1.0 && !sel[plan.tasks[t].node])) want[t] = 1;
+    if (ph.kind == kPhaseLeaf)
+      for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
+        if (f < 1.0 && !sel[plan.tasks[t].node]) want[t] = 1;
   if (split)
     for (const Phase& ph : plan.split_phases)
       for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t)
@@ -1968,7 +1995,7 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
     // rank's subtree part (SURVEY §8e fallback)
     Plan probe;
     std::string err;
-    if (!build_plan(*cds, kBM, probe, err)) return set_err(HMXG_EINVAL, err);
+    if (!build_plan(*cds, kBM, probe, err, plan_spec())) return set_err(HMXG_EINVAL, err);
     const std::uint64_t bytes = 8 * probe.tile_elems + sizeof(Task) * probe.tasks.size() +
                                 sizeof(SegDev) * probe.segs.size() + 4 * (probe.ipmap.size() + probe.idmap.size());
     std::uint64_t budget = ctx->comm.hbm_budget;
@@ -2147,7 +2174,9 @@ int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info) {
   // permute-in, eval_dag, permute-out; 1 when the last evaluation fused the permutations
   info->launches_per_eval = mat->devs.empty() ? 3 : mat->devs[0].last_launches;
   info->flops_per_col = 2.0 * (2.0 * p.v_elems + p.b_elems + p.d_elems);
-  for (const Phase& ph : p.phases) info->exec_flops_per_col += ph.flops_per_col;
+  for (const Phase* ph : tree_phases(p, 0)) info->exec_flops_per_col += ph->flops_per_col;
+  for (const Phase& ph : p.phases)
+    if (ph.kind == kPhaseLeaf) info->exec_flops_per_col += ph.flops_per_col;
   info->device_bytes = mat->devs.empty() ? 0 : mat->devs[0].resident_bytes;
   info->split_parts = p.nparts;
   info->part = p.part;

@@ -277,12 +277,12 @@ __global__ void __launch_bounds__(256) gen_near(const double* __restrict__ pts, 
 
 // ---------------------------------------------------------------- A pre-tiling
 __global__ void tile_a(const double* __restrict__ gd, const double* __restrict__ gb, const double* __restrict__ gv,
-                       const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,
+                       const double* __restrict__ gc, const TileSrc* __restrict__ srcs, const std::uint32_t* __restrict__ chunk_seg,
                        const std::uint32_t* __restrict__ maps, double* __restrict__ tiles, std::uint64_t nchunks) {
   for (std::uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const TileSrc s = srcs[chunk_seg[c]];
     const std::uint64_t chunk_in_seg = (c * kChunkElems - s.tile_off) / kChunkElems;
-    const double* a = (s.gen == kGenD ? gd : (s.gen == kGenB ? gb : gv)) + s.a_off;
+    const double* a = (s.gen == kGenD ? gd : (s.gen == kGenB ? gb : (s.gen == kGenV ? gv : gc))) + s.a_off;
     double* out = tiles + c * kChunkElems;
     for (int e = threadIdx.x; e < kChunkElems; e += blockDim.x) {
       int k, r;

@@ -609,6 +609,163 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   };
   if (near_end > near_begin) split_phase(kPhaseNear, near_begin, near_end);
   if (acc_end > near_end) split_phase(kPhaseLeaf, near_end, acc_end);
+
+  // --- flat tree for small trees (Plan::flat_phases). A chain of dependent GEMM levels costs
+  //     ~4 us each through the DAG's gpu-scope counters (cfg1: 11 levels, the whole step),
+  //     while a small tree's transfer products are cheap to form once. So every active
+  //     internal node's T is taken straight from its leaves' T, T_p = sum_l C_pl T_l with
+  //     C_pl = M_p,c C_cl (M_p = V_p^T, its column block of the child c on the path; C_ll = I),
+  //     and every leaf's S straight from the T's it depends on,
+  //     S_l = sum_{a on the path} sum_{j far from a} (G_la B_aj) T_j with G_ll = I and
+  //     G_l,parent(a) = G_la V_parent(a)[rows of a] (executor.cpp:51-110 unrolled). Two
+  //     dependent levels replace the internal upward and far+downward ones. The composites
+  //     are formed once on the host in FP64, in the nodes' T/S row orders, as generator kGenC.
+  //     Used when the tree is small and the extra multiply-adds stay below a quarter of the
+  //     evaluation's (plan-wide, so every column count gives the same bits).
+  // (the composites read B and V on the host: not with far blocks generated on the device)
+  if (!splitting && split.flat_tree && !split.generated_far && (v.bgen || !v.num_far) && v.vgen) {
+    std::vector<std::vector<std::uint32_t>> leaves_under(nn);
+    for (std::size_t qi = order.size(); qi-- > 0;) {  // children before parents
+      const std::uint32_t i = order[qi];
+      if (!active(i)) continue;
+      if (is_leaf(i)) {
+        leaves_under[i] = {i};
+        continue;
+      }
+      for (std::uint32_t c : {v.lchild[i], v.rchild[i]})
+        if (active(c)) leaves_under[i].insert(leaves_under[i].end(), leaves_under[c].begin(), leaves_under[c].end());
+    }
+    double flat = 0.0, replaced = 0.0, total = 0.0;
+    for (const Phase& ph : plan.phases) {
+      if (ph.kind == kPhaseLeaf) {
+        total += ph.flops_per_col;
+        continue;
+      }
+      total += ph.flops_per_col;
+      if (!(ph.kind == kPhaseUp && ph.level == 0)) replaced += ph.flops_per_col;
+    }
+    for (std::uint32_t i = 0; i < nn; ++i)
+      if (active(i) && !is_leaf(i))
+        for (std::uint32_t l : leaves_under[i]) flat += 2.0 * v.sranks[i] * v.sranks[l];
+    for (std::uint32_t l = 0; l < nn; ++l) {
+      if (!active(l) || !is_leaf(l)) continue;
+      for (std::uint32_t a = l;;) {
+        for (std::uint64_t s : far_of[a]) flat += 2.0 * v.sranks[l] * v.sranks[v.far_pairs[2 * s + 1]];
+        const std::uint32_t par = v.parent[a];
+        if (par == HMXG_NO_NODE || !active(par)) break;
+        a = par;
+      }
+    }
+    const bool small = v.n <= 65536 && nn <= 1024;
+    if (small && flat - replaced <= 0.25 * total && replaced > 0.0) {
+      // dense r_a x r_b blocks in the nodes' T/S row orders (column major), appended to cgen
+      auto vget = [&](std::uint32_t p, std::uint64_t row, std::uint64_t col) {
+        return v.vgen[v.vptr[vslot[p]] + row + col * v_width(p)];
+      };
+      std::vector<std::vector<std::pair<std::uint32_t, std::vector<double>>>> comp(nn);  // C_pl, old orders
+      for (std::size_t qi = order.size(); qi-- > 0;) {
+        const std::uint32_t p = order[qi];
+        if (!active(p) || is_leaf(p)) continue;
+        const std::uint32_t rp = v.sranks[p];
+        for (std::uint32_t c : {v.lchild[p], v.rchild[p]}) {
+          if (!active(c)) continue;
+          const std::uint64_t off = c == v.lchild[p] ? 0 : v.sranks[v.lchild[p]];
+          const std::uint32_t rc = v.sranks[c];
+          auto mpc = [&](std::uint32_t i, std::uint32_t k) { return vget(p, off + k, i); };  // M_p,c(i, k)
+          if (is_leaf(c)) {
+            std::vector<double> m(std::size_t(rp) * rc);
+            for (std::uint32_t k = 0; k < rc; ++k)
+              for (std::uint32_t i = 0; i < rp; ++i) m[i + std::size_t(k) * rp] = mpc(i, k);
+            comp[p].push_back({c, std::move(m)});
+          } else {
+            for (const auto& [l, ccl] : comp[c]) {
+              const std::uint32_t rl = v.sranks[l];
+              std::vector<double> m(std::size_t(rp) * rl, 0.0);
+              for (std::uint32_t b = 0; b < rl; ++b)
+                for (std::uint32_t k = 0; k < rc; ++k) {
+                  const double x = ccl[k + std::size_t(b) * rc];
+                  if (x == 0.0) continue;
+                  for (std::uint32_t i = 0; i < rp; ++i) m[i + std::size_t(b) * rp] += mpc(i, k) * x;
+                }
+              comp[p].push_back({l, std::move(m)});
+            }
+          }
+        }
+      }
+      // a block in new row / column orders into cgen: A(r', c') = M(oldrow(ra, r'), oldrow(cb, c'))
+      auto put = [&](std::uint32_t ra, std::uint32_t cb, const std::vector<double>& m) {
+        const std::uint32_t R = v.sranks[ra], K = v.sranks[cb];
+        const std::uint64_t off = plan.cgen.size();
+        plan.cgen.resize(off + std::uint64_t(R) * K);
+        for (std::uint32_t c2 = 0; c2 < K; ++c2)
+          for (std::uint32_t r2 = 0; r2 < R; ++r2)
+            plan.cgen[off + r2 + std::uint64_t(c2) * R] = m[oldrow(ra, r2) + std::size_t(oldrow(cb, c2)) * R];
+        return off;
+      };
+      cur_id.clear();
+      cur_id_node0 = cur_id_node1 = kNoMap;
+      // flat upward: every active internal node from its leaves
+      Phase up{kPhaseUp, 0, static_cast<std::uint32_t>(plan.tasks.size()), 0, 1, 0.0, 0.0, 0.0};
+      for (std::uint32_t p : order) {
+        if (!active(p) || is_leaf(p)) continue;
+        std::vector<std::pair<std::uint32_t, std::uint64_t>> blocks;  // (leaf, cgen offset)
+        for (const auto& [l, m] : comp[p]) blocks.push_back({l, put(p, l, m)});
+        cur_node = p;
+        add_tiles(v.sranks[p], kBufT, plan.node_off[p], [&](std::uint32_t r0, std::uint32_t m) {
+          for (const auto& [l, co] : blocks)
+            push_seg(kGenC, false, co, v.sranks[p], v.sranks[l], m, kBufT, plan.node_off[l], l, r0, kNoMap, kNoMap, m);
+        }, up);
+      }
+      up.task_end = static_cast<std::uint32_t>(plan.tasks.size());
+      // flat far+downward: every active leaf's S from the T's of the far partners on its path
+      Phase down{kPhaseDown, 0, static_cast<std::uint32_t>(plan.tasks.size()), 0, 1, 0.0, 0.0, 0.0};
+      for (std::uint32_t l : order) {
+        if (!active(l) || !is_leaf(l)) continue;
+        const std::uint32_t rl = v.sranks[l];
+        std::vector<double> g(std::size_t(rl) * rl, 0.0);  // G_la, r_l x r_a, old orders
+        for (std::uint32_t r = 0; r < rl; ++r) g[r + std::size_t(r) * rl] = 1.0;
+        std::vector<std::pair<std::uint32_t, std::uint64_t>> blocks;  // (partner j, cgen offset)
+        for (std::uint32_t a = l;;) {
+          const std::uint32_t ra = v.sranks[a];
+          for (std::uint64_t s : far_of[a]) {
+            const std::uint32_t j = v.far_pairs[2 * s + 1], rj = v.sranks[j];
+            const double* B = v.bgen + v.bptr[s];  // r_a x r_j, column major
+            std::vector<double> m(std::size_t(rl) * rj, 0.0);
+            for (std::uint32_t b = 0; b < rj; ++b)
+              for (std::uint32_t k = 0; k < ra; ++k) {
+                const double x = B[k + std::size_t(b) * ra];
+                if (x == 0.0) continue;
+                for (std::uint32_t i = 0; i < rl; ++i) m[i + std::size_t(b) * rl] += g[i + std::size_t(k) * rl] * x;
+              }
+            blocks.push_back({j, put(l, j, m)});
+          }
+          const std::uint32_t par = v.parent[a];
+          if (par == HMXG_NO_NODE || !active(par)) break;
+          const std::uint64_t off = a == v.lchild[par] ? 0 : v.sranks[v.lchild[par]];
+          const std::uint32_t rp = v.sranks[par];
+          std::vector<double> g2(std::size_t(rl) * rp, 0.0);  // G_l,par = G_la V_par[rows of a]
+          for (std::uint32_t b = 0; b < rp; ++b)
+            for (std::uint32_t k = 0; k < ra; ++k) {
+              const double x = vget(par, off + k, b);
+              if (x == 0.0) continue;
+              for (std::uint32_t i = 0; i < rl; ++i) g2[i + std::size_t(b) * rl] += g[i + std::size_t(k) * rl] * x;
+            }
+          g.swap(g2);
+          a = par;
+        }
+        cur_node = l;
+        add_tiles(rl, kBufS, plan.node_off[l], [&](std::uint32_t r0, std::uint32_t m) {
+          for (const auto& [j, co] : blocks)
+            push_seg(kGenC, false, co, rl, v.sranks[j], m, kBufT, plan.node_off[j], j, r0, kNoMap, kNoMap, m);
+        }, down);
+      }
+      down.task_end = static_cast<std::uint32_t>(plan.tasks.size());
+      if (up.task_end > up.task_begin) plan.flat_phases.push_back(up);
+      if (down.task_end > down.task_begin) plan.flat_phases.push_back(down);
+      plan.flat = !plan.flat_phases.empty();
+      plan.flat_extra_flops_per_col = flat - replaced;
+    }
+  }
   if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: too many GEMM segments");
   return true;

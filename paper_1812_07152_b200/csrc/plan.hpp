@@ -35,7 +35,7 @@ constexpr std::uint32_t kRowAlign = 16;  // = the kernel's K chunk
 // Operand buffers a task can read (B side) or write (C side).
 enum Buf : std::uint16_t { kBufWp = 0, kBufT = 1, kBufS = 2, kBufYp = 3, kNumBufs = 4 };
 // Generator arrays an A operand is tiled from.
-enum Gen : std::uint8_t { kGenD = 0, kGenB = 1, kGenV = 2 };
+enum Gen : std::uint8_t { kGenD = 0, kGenB = 1, kGenV = 2, kGenC = 3 /* Plan::cgen composites */ };
 
 // Source of one pre-tiled A operand: rows [0, m) of the tile, K columns, from generator
 // `gen` at element offset a_off, column major with leading dimension lda; with `trans`
@@ -161,6 +161,12 @@ struct Plan {
   std::vector<std::uint32_t> idmap;
   double identity_flops_per_col = 0.0;  // multiply-adds by exact 0/1 rows the kernel skips
   bool near_otf = false;                 // near blocks generated per evaluation (hmxg_upload_generated_ex)
+  // flat tree (small trees, plan.cpp): the internal upward and far+downward levels replaced by
+  // two phases of composite transfer products (kGenC blocks in cgen)
+  bool flat = false;
+  std::vector<Phase> flat_phases;
+  std::vector<double> cgen;
+  double flat_extra_flops_per_col = 0.0;
   mutable double ct_dmma = -1.0;         // CTree work per 8-column octet in DMMAs (hmxg.cu, cached)
   mutable std::uint64_t ct_smem = 0;     // its tables' shared-memory bytes
 };
@@ -178,6 +184,7 @@ struct SplitSpec {
   bool identity_rows = true;    // lower the bases' unit rows to row copies (plan.cpp)
   bool generated_near = false;  // dgen may be null: the near blocks are generated on the device
   bool generated_far = false;   // bgen may be null: the far blocks are generated on the device
+  bool flat_tree = true;        // small trees: composite (flat) tree phases, see Plan::flat_phases
 };
 bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::string& err,
                 const SplitSpec& split = {});

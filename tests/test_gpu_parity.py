@@ -428,6 +428,7 @@ def test_ctree_mode_gives_the_dag_bits(name, q, monkeypatch):
     and the level launches, through the host and the device paths, for 2, 4 and 8-CTA clusters."""
     import torch
 
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")  # CTree runs the level-by-level tree
     if name == "tiny":
         inst = build_instance(InstanceSpec(n=129, d=3, leaf=16, max_rank=12, seed=3))
     elif name == "ragged":

@@ -29,7 +29,10 @@ def test_subtree_split_fallback_through_shim():
     """hmx_gpu::Evaluator(cds, device, hmxg_comm) with an HBM budget the CDS exceeds: two
     ranks hold one subtree part each and evaluate collectively, bit-identical to the
     replicated evaluation; a failing collective is HMXG_ECOMM (tests/cpp/test_split_gpu.cpp)."""
-    out = subprocess.run([SPLIT_BIN], capture_output=True, text=True, timeout=600)
+    # bit-identity split vs replicated holds for the level-by-level tree (the split runs it;
+    # replicated small trees run the flat tree by default, equal to rounding)
+    out = subprocess.run([SPLIT_BIN], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "HMXG_NO_FLAT": "1"})
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "split checks passed" in out.stdout

@@ -17,9 +17,12 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name,nparts,q", [("cfg1-hss", 2, 64), ("cfg2-h2b", 3, 70), ("cfg2-h2b", 4, 128)])
-def test_split_parts_equal_single_device(name, nparts, q):
+def test_split_parts_equal_single_device(name, nparts, q, monkeypatch):
+    """(The split runs the level-by-level tree; the single-device reference here does too:
+    small trees otherwise run the flat tree, equal to rounding, checked at the end.)"""
     import torch
 
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
     spec, _ = config(name)
     inst = build_instance(spec)
     n = inst.cds.n
@@ -38,6 +41,11 @@ def test_split_parts_equal_single_device(name, nparts, q):
     assert max(part_bytes) < full_bytes
     for p in parts:
         p.close()
+    monkeypatch.delenv("HMXG_NO_FLAT")
+    ev_flat = Evaluator(inst.cds)  # the default replicated upload (flat tree for small trees)
+    y_flat = torch.empty_like(w)
+    ev_flat.evaluate_device(w.data_ptr(), y_flat.data_ptr(), q, sync=True, stream=torch_stream())
+    assert oracle.rel_frob(y_flat.cpu().numpy().T, yn) <= 1e-13
 
 
 def test_split_tau_instance_and_reference():

@@ -293,8 +293,11 @@ def test_cds_fingerprint_sees_every_edit():
 def test_dag_check_ctree_mode(monkeypatch):
     """CTree mode (HMXG_CTREE=1): the item list is the near tiles only (x column blocks x
     parts), and the CTree levels hold every other task of the split variant once, each level
-    reading only rows of earlier levels (hmxg_dag_check's CTree branch)."""
+    reading only rows of earlier levels (hmxg_dag_check's CTree branch). (CTree runs the
+    level-by-level tree: the flat tree of small trees is off.)"""
     from paper_1812_07152_b200 import config
+
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
 
     insts = [build_instance(config("cfg1-hss")[0]), _small(),
              build_instance(InstanceSpec(n=1500, d=5, leaf=40, max_rank=24, mode="budget", budget=0.1, seed=9))]
