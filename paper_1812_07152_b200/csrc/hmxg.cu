@@ -67,6 +67,7 @@ struct DevState {
   std::vector<cudaEvent_t> phase_ev;  // launches + 1
   bool phase_valid = false;
   double* tiles = nullptr;  // pre-tiled A operands
+  std::uint64_t tile_elems = 0;
   Task* tasks = nullptr;
   SegDev* segs = nullptr;
   std::uint32_t* ipmap = nullptr;
@@ -919,6 +920,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       dp.pmap = d.pmap;
       dp.reset_words = static_cast<std::uint32_t>(words);
       dp.exit_ctr = d.dag_done + words;
+      dp.pf_tile_lines = d.tile_elems / 16;
       p.y_final = y;
       p.ldy = ldy;
       p.pmap = d.pmap;
@@ -1469,6 +1471,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
     HMXG_TRY(dev_upload(&cseg, tcseg.data(), tcseg.size(), d.comp));
     std::uint32_t* maps = nullptr;
     HMXG_TRY(dev_upload(&maps, plan.maps.data(), plan.maps.size(), d.comp));
+    d.tile_elems = tile_elems;
     if (tile_elems) {
       HMXG_CUDA(cudaMalloc(&d.tiles, tile_elems * sizeof(double)));
       const std::uint64_t nch = tcseg.size();

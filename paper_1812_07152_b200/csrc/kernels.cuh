@@ -844,6 +844,7 @@ struct DagParams {
   // as they are (the split fallback's stage 0, whose T counters stage 1 reads).
   std::uint32_t reset_words;
   std::uint32_t* exit_ctr;
+  std::uint64_t pf_tile_lines;  // fused mode: 128-byte lines of the A chunks prefetched into L2 first
   // CTree mode (small problems, fused): every task but the near field runs inside clusters of
   // ct_csize CTAs, one cluster per 8-column octet of W (the first ct_noct * ct_csize CTAs),
   // level by level with cluster barriers in between; the item list holds the near tiles only.
@@ -1286,6 +1287,18 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
   const bool ct_cta = kNarrow && blockIdx.x < ct_ctas;
   if (kNarrow && ct_cta) ct_run(p, d, c, blockIdx.x / d.ct_csize, blockIdx.x % d.ct_csize, done_y, done_w, cst, wmul);
 
+  if (kNarrow && d.fused && d.pf_tile_lines) {
+    // Small problems start cold (an L2 flush, or just the previous evaluation's traffic):
+    // every CTA sends a share of the A chunks and of W to L2 first, so each level's first
+    // loads hit L2 instead of paying a DRAM round trip on the critical chain.
+    const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const std::uint64_t nt = static_cast<std::uint64_t>(gridDim.x) * kThreads;
+    for (std::uint64_t l = tid; l < d.pf_tile_lines; l += nt)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.tiles + l * 16));
+    const std::uint64_t wl = (static_cast<std::uint64_t>(d.n) + 15) / 16;  // lines per column of W
+    for (std::uint64_t l = tid; l < wl * p.q; l += nt)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(d.w + (l % wl) * 16 + (l / wl) * d.ldw));
+  }
   if (kNarrow && d.fused && warp < kConsumerWarps) {
     // Wp[ipmap[r]][phys(c)] = W[r + c ldw] in source order: a job is 32 consecutive points x
     // one column block, read as whole 256-byte column segments, transposed through shared

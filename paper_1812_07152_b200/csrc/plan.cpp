@@ -624,17 +624,6 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   //     evaluation's (plan-wide, so every column count gives the same bits).
   // (the composites read B and V on the host: not with far blocks generated on the device)
   if (!splitting && split.flat_tree && !split.generated_far && (v.bgen || !v.num_far) && v.vgen) {
-    std::vector<std::vector<std::uint32_t>> leaves_under(nn);
-    for (std::size_t qi = order.size(); qi-- > 0;) {  // children before parents
-      const std::uint32_t i = order[qi];
-      if (!active(i)) continue;
-      if (is_leaf(i)) {
-        leaves_under[i] = {i};
-        continue;
-      }
-      for (std::uint32_t c : {v.lchild[i], v.rchild[i]})
-        if (active(c)) leaves_under[i].insert(leaves_under[i].end(), leaves_under[c].begin(), leaves_under[c].end());
-    }
     double flat = 0.0, replaced = 0.0, total = 0.0;
     for (const Phase& ph : plan.phases) {
       if (ph.kind == kPhaseLeaf) {
@@ -644,9 +633,49 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       total += ph.flops_per_col;
       if (!(ph.kind == kPhaseUp && ph.level == 0)) replaced += ph.flops_per_col;
     }
+    // Frontier of an upward composite: the nodes whose T it multiplies. Single stage: the
+    // leaves. With a middle height h_mid, the nodes above it start from the nodes at h_mid
+    // (one more dependent level, but the top nodes' K -- a segment per leaf under them -- is
+    // cut: cfg1's root children stream 32 chunks from 16 leaves, 12 from 4 mid nodes).
+    auto frontier_of = [&](std::uint32_t p, std::uint32_t h_mid, auto&& self) -> std::vector<std::uint32_t> {
+      std::vector<std::uint32_t> f;
+      for (std::uint32_t c : {v.lchild[p], v.rchild[p]}) {
+        if (!active(c)) continue;
+        if (is_leaf(c) || (h_mid && sub_h[c] == h_mid)) {
+          f.push_back(c);
+        } else {
+          const std::vector<std::uint32_t> g = self(c, h_mid, self);
+          f.insert(f.end(), g.begin(), g.end());
+        }
+      }
+      return f;
+    };
+    auto kchunks = [&](std::uint32_t p, std::uint32_t h_mid) {
+      std::uint64_t k = 0;
+      for (std::uint32_t f : frontier_of(p, (h_mid && sub_h[p] > h_mid) ? h_mid : 0, frontier_of))
+        k += (v.sranks[f] + kRowAlign - 1) / kRowAlign;
+      return k;
+    };
+    std::uint32_t h_mid = 0;
+    {
+      std::uint64_t best = 0;
+      for (std::uint32_t i = 0; i < nn; ++i)
+        if (active(i) && !is_leaf(i)) best = std::max(best, kchunks(i, 0));
+      if (best > 16)
+        for (std::uint32_t h = 1; h + 1 <= max_h; ++h) {
+          std::uint64_t worst = 0;
+          for (std::uint32_t i = 0; i < nn; ++i)
+            if (active(i) && !is_leaf(i)) worst = std::max(worst, kchunks(i, h));
+          if (worst < best) {
+            best = worst;
+            h_mid = h;
+          }
+        }
+    }
+    auto stage_mid = [&](std::uint32_t p) { return (h_mid && sub_h[p] > h_mid) ? h_mid : 0u; };
     for (std::uint32_t i = 0; i < nn; ++i)
       if (active(i) && !is_leaf(i))
-        for (std::uint32_t l : leaves_under[i]) flat += 2.0 * v.sranks[i] * v.sranks[l];
+        for (std::uint32_t f : frontier_of(i, stage_mid(i), frontier_of)) flat += 2.0 * v.sranks[i] * v.sranks[f];
     for (std::uint32_t l = 0; l < nn; ++l) {
       if (!active(l) || !is_leaf(l)) continue;
       for (std::uint32_t a = l;;) {
@@ -662,8 +691,14 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       auto vget = [&](std::uint32_t p, std::uint64_t row, std::uint64_t col) {
         return v.vgen[v.vptr[vslot[p]] + row + col * v_width(p)];
       };
-      std::vector<std::vector<std::pair<std::uint32_t, std::vector<double>>>> comp(nn);  // C_pl, old orders
+      // C_pf over each node's frontier, old orders: comp[0] = from the leaves, comp[1] = from
+      // the leaves and the nodes at h_mid (used above h_mid)
+      std::vector<std::vector<std::pair<std::uint32_t, std::vector<double>>>> comps[2] = {
+          std::vector<std::vector<std::pair<std::uint32_t, std::vector<double>>>>(nn),
+          std::vector<std::vector<std::pair<std::uint32_t, std::vector<double>>>>(h_mid ? nn : 0)};
+      for (int st = 0; st < (h_mid ? 2 : 1); ++st)
       for (std::size_t qi = order.size(); qi-- > 0;) {
+        auto& comp = comps[st];
         const std::uint32_t p = order[qi];
         if (!active(p) || is_leaf(p)) continue;
         const std::uint32_t rp = v.sranks[p];
@@ -672,7 +707,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
           const std::uint64_t off = c == v.lchild[p] ? 0 : v.sranks[v.lchild[p]];
           const std::uint32_t rc = v.sranks[c];
           auto mpc = [&](std::uint32_t i, std::uint32_t k) { return vget(p, off + k, i); };  // M_p,c(i, k)
-          if (is_leaf(c)) {
+          if (is_leaf(c) || (st == 1 && sub_h[c] == h_mid)) {
             std::vector<double> m(std::size_t(rp) * rc);
             for (std::uint32_t k = 0; k < rc; ++k)
               for (std::uint32_t i = 0; i < rp; ++i) m[i + std::size_t(k) * rp] = mpc(i, k);
@@ -704,19 +739,25 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
       };
       cur_id.clear();
       cur_id_node0 = cur_id_node1 = kNoMap;
-      // flat upward: every active internal node from its leaves
-      Phase up{kPhaseUp, 0, static_cast<std::uint32_t>(plan.tasks.size()), 0, 1, 0.0, 0.0, 0.0};
-      for (std::uint32_t p : order) {
-        if (!active(p) || is_leaf(p)) continue;
-        std::vector<std::pair<std::uint32_t, std::uint64_t>> blocks;  // (leaf, cgen offset)
-        for (const auto& [l, m] : comp[p]) blocks.push_back({l, put(p, l, m)});
-        cur_node = p;
-        add_tiles(v.sranks[p], kBufT, plan.node_off[p], [&](std::uint32_t r0, std::uint32_t m) {
-          for (const auto& [l, co] : blocks)
-            push_seg(kGenC, false, co, v.sranks[p], v.sranks[l], m, kBufT, plan.node_off[l], l, r0, kNoMap, kNoMap, m);
-        }, up);
+      // flat upward: the active internal nodes up to h_mid (all of them without one) from their
+      // leaves, then those above it from the nodes at h_mid
+      Phase ups[2];
+      for (int st = 0; st < (h_mid ? 2 : 1); ++st) {
+        Phase& up = ups[st];
+        up = Phase{kPhaseUp, 0, static_cast<std::uint32_t>(plan.tasks.size()), 0, static_cast<std::uint32_t>(1 + st),
+                   0.0, 0.0, 0.0};
+        for (std::uint32_t p : order) {
+          if (!active(p) || is_leaf(p) || (stage_mid(p) != 0) != (st == 1)) continue;
+          std::vector<std::pair<std::uint32_t, std::uint64_t>> blocks;  // (frontier node, cgen offset)
+          for (const auto& [f, m] : comps[st][p]) blocks.push_back({f, put(p, f, m)});
+          cur_node = p;
+          add_tiles(v.sranks[p], kBufT, plan.node_off[p], [&](std::uint32_t r0, std::uint32_t m) {
+            for (const auto& [f, co] : blocks)
+              push_seg(kGenC, false, co, v.sranks[p], v.sranks[f], m, kBufT, plan.node_off[f], f, r0, kNoMap, kNoMap, m);
+          }, up);
+        }
+        up.task_end = static_cast<std::uint32_t>(plan.tasks.size());
       }
-      up.task_end = static_cast<std::uint32_t>(plan.tasks.size());
       // flat far+downward: every active leaf's S from the T's of the far partners on its path
       Phase down{kPhaseDown, 0, static_cast<std::uint32_t>(plan.tasks.size()), 0, 1, 0.0, 0.0, 0.0};
       for (std::uint32_t l : order) {
@@ -760,8 +801,10 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
         }, down);
       }
       down.task_end = static_cast<std::uint32_t>(plan.tasks.size());
-      if (up.task_end > up.task_begin) plan.flat_phases.push_back(up);
+      for (int st = 0; st < (h_mid ? 2 : 1); ++st)
+        if (ups[st].task_end > ups[st].task_begin) plan.flat_phases.push_back(ups[st]);
       if (down.task_end > down.task_begin) plan.flat_phases.push_back(down);
+      plan.flat_mid_height = h_mid;
       plan.flat = !plan.flat_phases.empty();
       plan.flat_extra_flops_per_col = flat - replaced;
     }

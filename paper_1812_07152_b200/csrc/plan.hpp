@@ -167,6 +167,7 @@ struct Plan {
   std::vector<Phase> flat_phases;
   std::vector<double> cgen;
   double flat_extra_flops_per_col = 0.0;
+  std::uint32_t flat_mid_height = 0;  // 0: one flat upward phase from the leaves
   mutable double ct_dmma = -1.0;         // CTree work per 8-column octet in DMMAs (hmxg.cu, cached)
   mutable std::uint64_t ct_smem = 0;     // its tables' shared-memory bytes
 };
