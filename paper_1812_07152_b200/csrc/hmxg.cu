@@ -386,10 +386,17 @@ std::uint32_t colsplit(const Plan& plan, std::size_t q, unsigned grid, std::uint
 #ifndef HMXG_SPLIT_FRAC
 #define HMXG_SPLIT_FRAC 0.0
 #endif
+// Default f by work items per CTA of the combined variant (below 48 the whole split variant
+// runs): measured on cfg5-HSS, the 8-GPU sweep's per-rank workloads -- Q=256 (83 items per
+// CTA) 2.189 -> 2.162 ms at f = 0.2-0.35, Q=512 (165) 4.232 -> 4.219 ms at f = 0.2, Q=1024
+// (330) and Q=2048 best at 0 (profiles/r02/split_frac_sweep.txt): f = 0.3 (1 - items / 250).
 double split_frac(const Plan& plan, std::size_t q, unsigned grid) {
   if (plan.split_phases.empty() || plan.near_otf || plan.nparts != 1) return 0.0;
   if (split_leaf(plan, q, grid)) return 1.0;
-  double f = HMXG_SPLIT_FRAC;
+  std::uint64_t tasks = 0;
+  for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
+  const double per_cta = double(tasks) * double((q + kBN - 1) / kBN) / std::max(1u, grid);
+  double f = HMXG_SPLIT_FRAC > 0.0 ? HMXG_SPLIT_FRAC : std::max(0.0, 0.3 * (1.0 - per_cta / 250.0));
   if (const char* e = std::getenv("HMXG_SPLIT_FRAC")) f = std::atof(e);
   return std::min(1.0, std::max(0.0, f));
 }
