@@ -1004,10 +1004,17 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     ++*launches;
     desc_perm(0);
     HMXG_TRY(mark());
-    const bool pdl = !time_phases;  // an event between two kernels would break the programmatic edge
+    // Programmatic dependent launch of eval_dag and permute_out (HMXG_PDL=1; 2: permute_out
+    // only) is off by default: measured on cfg5-HSS without per-launch events, 16.60 ms with
+    // it (either form) against 16.38-16.47 ms without -- the dependents' early CTAs hold SM
+    // slots through their predecessor's tail; cfg2 equal. (An event between two kernels would
+    // break the programmatic edge anyway.)
+    const bool pdl = !time_phases;
+    const int pdl_mode = std::getenv("HMXG_PDL") ? std::atoi(std::getenv("HMXG_PDL")) : 0;
+    const bool pdl_dag = pdl && pdl_mode == 1, pdl_out = pdl && pdl_mode >= 1;
     const bool narrow = dp.colsplit > 1 || dp.cstride > 1;
     if (grid) {  // (on the fly, a tree without levels has nothing for the DAG)
-      HMXG_TRY(launch_dependent(pdl, narrow ? eval_dag<true> : eval_dag<false>, dim3(grid), dim3(kThreads), kSmemBytes,
+      HMXG_TRY(launch_dependent(pdl_dag, narrow ? eval_dag<true> : eval_dag<false>, dim3(grid), dim3(kThreads), kSmemBytes,
                                 st, tm_wp, tm_t, tm_s, p, dp));
       ++*launches;
       DevState::LaunchDesc a{5, 0, 0, 0.0, 0.0, 0.0};
@@ -1022,7 +1029,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
       HMXG_TRY(mark());
     }
     if (plan.near_otf) HMXG_TRY(run_waves(d.tile_counters));
-    HMXG_TRY(launch_dependent(pdl && !plan.near_otf, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp),
+    HMXG_TRY(launch_dependent(pdl_out && !plan.near_otf, permute_out, pgrid2, eblk, 0, st, static_cast<const double*>(d.yp),
                               std::uint64_t(ldq), static_cast<const std::uint32_t*>(d.ipmap), y, std::uint64_t(ldy), n,
                               qq, d.dag_done, std::uint64_t(words + 1)));
     ++*launches;
