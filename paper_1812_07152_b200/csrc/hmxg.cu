@@ -1443,7 +1443,8 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       for (cudaEvent_t* e : {&d.ev_in[b], &d.ev_done[b], &d.ev_out[b]})
         HMXG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     HMXG_CUDA(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
-    d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + 3 + 2 * otf_l.waves.size());
+    d.phase_ev.resize(plan.phases.size() + plan.split_phases.size() + plan.flat_phases.size() + 3 +
+                      2 * otf_l.waves.size());
     for (auto& e : d.phase_ev) HMXG_CUDA(cudaEventCreate(&e));
     HMXG_CUDA(cudaFuncSetAttribute(grouped_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     HMXG_CUDA(cudaFuncSetAttribute(eval_dag<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -1463,8 +1464,10 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
 #define HMXG_GEMM_CTAS_PER_SM 3
 #endif
       d.gemm_grid = static_cast<unsigned>(std::max(1, std::min(per_sm, HMXG_GEMM_CTAS_PER_SM)) * sms);
-      HMXG_CUDA(cudaMalloc(&d.tile_counters, std::max<std::size_t>(1, plan.phases.size() + plan.split_phases.size() +
-                                                                          otf_l.waves.size()) * sizeof(std::uint32_t)));
+      HMXG_CUDA(cudaMalloc(&d.tile_counters,
+                           std::max<std::size_t>(1, plan.phases.size() + plan.split_phases.size() +
+                                                        plan.flat_phases.size() + otf_l.waves.size()) *
+                               sizeof(std::uint32_t)));
     }
     // raw generators -> pre-tiled A operands on the device, then the raw copies go away
     double *gd = nullptr, *gb = nullptr, *gv = nullptr;
