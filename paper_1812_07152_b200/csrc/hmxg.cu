@@ -1685,6 +1685,7 @@ int split_evaluate(hmxg_mat* mat, const double* W, std::size_t ldw, double* Y, s
   d.counters_dirty = false;
   d.last_fused = false;
   d.last_launches = *launches;
+  d.launch_desc.clear();  // (the subtree-split stages are not described per launch)
   if (!dev_ptrs) HMXG_TRY(copy_cols(Y, ldy, d.y_stage[0], n, n, q, cudaMemcpyDeviceToHost, st));
   if (!dev_ptrs || !(flags & HMXG_F_NO_SYNC)) {
     HMXG_CUDA(cudaStreamSynchronize(st));
