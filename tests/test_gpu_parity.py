@@ -457,3 +457,33 @@ def test_ctree_mode_gives_the_dag_bits(name, q, monkeypatch):
     assert oracle.rel_frob(dag, oracle.oracle_evaluate(inst.cds, w)) <= TOL
     ev.close()
     inst.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1-hss", "small", "uneven"])
+def test_flat_tree(name, monkeypatch):
+    """The flat tree of small trees (DESIGN.md kernel 6: the internal upward and far+downward
+    levels replaced by composite transfer products formed at upload) agrees with the level-by-
+    level tree (HMXG_NO_FLAT=1) to rounding and with the oracle; it is plan-wide, so a column
+    computed alone, in a 7-column shard or in the full block gives the same bits, and the DAG
+    equals the level launches bit for bit."""
+    if name == "small":  # (flat-eligible: n <= 65536, <= 1024 nodes, composites cheap)
+        inst = build_instance(InstanceSpec(n=2048, d=3, leaf=64, max_rank=32, seed=8, h=0.5))
+    elif name == "uneven":  # two-means tree, 3000 points: leaves of different sizes
+        inst = build_instance(InstanceSpec(n=3000, d=2, leaf=128, max_rank=40, seed=3, h=1.0, split="twomeans"))
+    else:
+        inst = build_instance(config(name)[0])
+    n, q = inst.cds.n, 64
+    w = _w(n, q, 29)
+    ev = Evaluator(inst.cds)
+    y = ev.evaluate(w)
+    assert np.array_equal(ev.evaluate(w, levels=True), y)
+    for c0, c1 in [(5, 6), (10, 17), (63, 64)]:
+        assert np.array_equal(ev.evaluate(np.asfortranarray(w[:, c0:c1])), y[:, c0:c1])
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    ev_levels = Evaluator(inst.cds)
+    y_levels = ev_levels.evaluate(w)
+    assert oracle.rel_frob(y, y_levels) <= 1e-13
+    assert oracle.rel_frob(y, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    ev.close()
+    ev_levels.close()
+    inst.close()
