@@ -93,6 +93,9 @@ struct DevState {
     std::uint32_t nitems = 0;
     std::uint32_t stage = 0;
     bool ct = false;  // CTree mode (near tiles only): the mode can change with the environment
+    // the slot holds a built list; the list itself can be empty (items == nullptr): a tree
+    // without levels whose near field is generated on the fly has nothing for the DAG
+    bool valid = false;
   };
   DagItems dag[4];                    // item lists of the last few (column count, stage) keys
   std::uint32_t dag_next = 0;
@@ -586,7 +589,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
                std::uint32_t stage = 0) {
   const bool ct = stage == 0 && ctree_csize(plan, q, d.gemm_grid) != 0;
   for (const auto& e : d.dag)
-    if (e.items && e.q == q && e.stage == stage && e.ct == ct) {
+    if (e.valid && e.q == q && e.stage == stage && e.ct == ct) {
       *out = &e;
       return HMXG_OK;
     }
@@ -595,7 +598,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   // call on another one), and the cached graph may have captured it
   HMXG_CUDA(cudaStreamSynchronize(st));
   if (d.pending) HMXG_CUDA(cudaEventSynchronize(d.ev_last));
-  if (e.items) d.drop_graph();
+  if (e.valid) d.drop_graph();
   cudaFree(e.items);
   e = DevState::DagItems{};
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage, d.gemm_grid);
@@ -672,6 +675,7 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   e.q = q;
   e.stage = stage;
   e.ct = ct;
+  e.valid = true;
   *out = &e;
   return HMXG_OK;
 }
@@ -888,7 +892,7 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     const DevState::DagItems* di = nullptr;
     const bool ct = ctree_csize(plan, q, d.gemm_grid) != 0;
     for (const auto& e : d.dag)
-      if (e.items && e.q == q && e.stage == 0 && e.ct == ct) di = &e;
+      if (e.valid && e.q == q && e.stage == 0 && e.ct == ct) di = &e;
     if (!di) return set_err(HMXG_ECUDA, "internal: DAG items not prepared");
     const std::uint32_t cst = counter_stride(plan, q, d.gemm_grid);
     const std::size_t words = dag_done_words(plan, q, cst);

@@ -105,3 +105,22 @@ def test_near_on_the_fly_equals_resident(kernel, h, mode, scratch_mb, monkeypatc
     assert oracle.rel_frob(y_res, oracle.oracle_evaluate(_pair(kernel, h, mode=mode, **kw)[0].cds, w)) <= TOL
     res.close()
     otf.close()
+
+
+@pytest.mark.gpu
+def test_near_on_the_fly_without_tree_levels():
+    """A tau tree whose blocks are all near (every rank 0) has no DAG items once the near field
+    runs in on-the-fly waves: the empty item list is a prepared list, not an error (found by
+    tests/test_gpu_fuzz.py), and repeated calls reuse it."""
+    spec = InstanceSpec(n=1184, d=5, kernel="exponential", h=0.5, leaf=33, mode="tau", tau=0.9, max_rank=24,
+                        split="kd", seed=11)
+    full = build_instance(spec)
+    assert int(full.cds.sranks.max()) == 0 and full.cds.num_far == 0
+    spec.skip_near = True
+    lean = build_instance(spec)
+    w = np.asfortranarray(np.random.default_rng(6).standard_normal((spec.n, 70)))
+    otf = Evaluator(lean.cds, points=lean.points(), kernel=Kernel("exponential", 0.5), near_on_the_fly=True)
+    y = otf.evaluate(w)
+    assert np.array_equal(otf.evaluate(w), y)
+    assert oracle.rel_frob(y, oracle.oracle_evaluate(full.cds, w)) <= TOL
+    otf.close()
