@@ -116,3 +116,53 @@ def test_random_instance_every_schedule(i, monkeypatch):
     res.close()
     lean.close()
     inst.close()
+
+
+def _ref_case(i: int) -> tuple["oracle.RefInstanceSpec", int]:
+    r = np.random.default_rng(5000 + i)
+    mode = int(r.integers(2))  # 0 tau / 1 hss
+    leaf = int(r.choice([8, 16, 24, 64, 128]))
+    n = int(r.integers(2 * leaf, min(60 * leaf, 5000)))
+    spec = oracle.RefInstanceSpec(n=n, d=int(r.choice([2, 3, 8, 32])), shape=int(r.integers(3)), mode=mode,
+                                  tau=float(r.choice([0.4, 0.65, 0.9])) if mode == 0 else 0.0, leaf=leaf,
+                                  kernel=0, h=float(r.choice([0.3, 1.0, 4.0])), bacc=float(r.choice([1e-3, 1e-5, 1e-9])),
+                                  max_rank=int(r.choice([8, 24, 64])), p=int(r.choice([1, 4, 8])),
+                                  near_bs=int(r.choice([1, 2, 4])), far_bs=int(r.choice([1, 4, 8])),
+                                  seed=int(r.integers(1, 1 << 20)))
+    q = int(r.choice([1, 5, 64, 70, 130, 300, 700]))
+    return spec, q
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_random_reference_instance(i):
+    """Instances the reference's own pipeline builds (tst::make_instance: its tree, interaction
+    lists, sampling, compress, blocking with random block sizes, coarsening for a random p,
+    build_cds), evaluated by the reference library (hmx::evaluate, and evaluate_reference on the
+    CompressedMatrix) and by the B200 through strided host buffers (ldw, ldy > n) and strided
+    device buffers; Q up to 700 runs the host path's multi-chunk pipeline."""
+    import torch
+
+    spec, q = _ref_case(i)
+    ri = oracle.RefInstance(spec)
+    n = ri.cds.n
+    w = oracle.random_matrix(n, q, 100 + i)
+    y_ref = ri.evaluate(w)
+    ev = Evaluator(ri.cds)
+    y = ev.evaluate(w)
+    assert oracle.rel_frob(y, y_ref) <= TOL, (i, spec)
+    assert oracle.rel_frob(y, ri.evaluate_reference(w)) <= 1e-12, (i, spec)
+    ld = n + 3 + i % 5
+    wbuf = np.full((q, ld), np.nan)  # row c holds column c of W, then padding
+    wbuf[:, :n] = w.T
+    ybuf = np.full((q, ld + 2), np.nan)
+    ev.evaluate_host_ptr(wbuf.ctypes.data, ybuf.ctypes.data, q, ldw=ld, ldy=ld + 2)
+    assert np.array_equal(ybuf[:, :n].T, y), (i, "strided host buffers")
+    assert np.isnan(ybuf[:, n:]).all()  # nothing written past a column's n rows
+    wd = torch.from_numpy(wbuf).cuda()
+    yd = torch.full((q, ld + 2), float("nan"), dtype=torch.float64, device="cuda")
+    ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, ldw=ld, ldy=ld + 2, stream=torch_stream(), sync=True)
+    yh = yd.cpu().numpy()
+    assert np.array_equal(yh[:, :n].T, y), (i, "strided device buffers")
+    assert np.isnan(yh[:, n:]).all()
+    ev.close()
+    ri.close()
