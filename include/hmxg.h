@@ -194,6 +194,10 @@ int hmxg_cds_fingerprint(const hmxg_cds_view* cds, uint64_t* out);
  * rows, the split leaf tasks' near rows) comes before it, and the completion targets equal
  * the writer tile counts. These are what eval_dag's deadlock freedom rests on. */
 int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* nitems);
+/* The claim order itself (host only, diagnostics and tests): up to `cap` work-item words into
+ * `items` (task index in bits 0-31, column block in bits 32-47, column-split part in 48-55),
+ * the total count into *nitems. */
+int hmxg_dag_items(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* items, size_t cap, uint64_t* nitems);
 int hmxg_info_get(const hmxg_mat* mat, hmxg_info* info);
 
 /* Subtree-split fallback for a CDS larger than one GPU's HBM. Part `part` of

@@ -193,6 +193,8 @@ HMXG_SYMBOLS = {
     "hmxg_validate": (C.c_int, [C.POINTER(CdsView), C.POINTER(Info)]),
     "hmxg_cds_fingerprint": (C.c_int, [C.POINTER(CdsView), C.POINTER(C.c_uint64)]),
     "hmxg_dag_check": (C.c_int, [C.POINTER(CdsView), C.c_size_t, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "hmxg_dag_items": (C.c_int, [C.POINTER(CdsView), C.c_size_t, C.c_uint32, C.POINTER(C.c_uint64), C.c_size_t,
+                                C.POINTER(C.c_uint64)]),
     "hmxg_info_get": (C.c_int, [C.c_void_p, C.POINTER(Info)]),
     "hmxg_evaluate": (
         C.c_int,

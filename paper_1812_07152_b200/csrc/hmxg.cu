@@ -418,6 +418,44 @@ std::vector<std::uint8_t> split_set(const Plan& plan, double f) {
     if (f >= 1.0 || std::floor((k + 1) * f) > std::floor(k * f)) sel[cand[k]] = 1;
   return sel;
 }
+// Subtree-pipelined claim order (wide DAGs that run the combined leaf tasks). The far+downward
+// levels next to the leaves are bound by HBM, not by the FP64 pipe -- their items are a few
+// chunks of K, mostly row traffic of T and S, which do not fit in L2 (cfg5-HSS: L8-L10 at 22-26
+// TF/s, within ~25% of their T/S bytes at HBM speed) -- while the leaf rows are bound by the FP64
+// pipe with HBM mostly idle. Level by level the two kinds never meet. The nodes below depth d0
+// are therefore grouped by their ancestor at depth d0 and the groups pipelined: the
+// far+downward levels of group g are interleaved (by estimated work, task by task, so a task's
+// column blocks stay consecutive and reuse its A chunks from L2) with the leaf rows of group
+// g-1; the upward pass and the levels above d0 run level by level as before. Every sequence
+// keeps its own level order and everything an item reads is emitted before it, so the order
+// stays topological (hmxg_dag_check) and the results are the same bits.
+// Measured (cfg5-HSS eval_dag, tools/pipe_check.py): Q=2048 13.43 -> 13.32 ms at d0 = 2 (13.34
+// at 3, 13.39 at 4), Q=1536 10.09 -> 10.05, Q=1024 6.79 -> 6.81 (below the threshold now); the
+// H2-b configs unchanged. The same pipelining of the upward levels with the next group's
+// leaf-upward tasks lost (13.45 at d0 = 2, 13.54 at 4: both sides read HBM heavily) and was
+// dropped. Returns d0, or 0 for the level-major order. HMXG_PIPE sets d0 (0: off),
+// HMXG_PIPE_MIN the work items per CTA from which the order applies (tests).
+#ifndef HMXG_PIPE_DEPTH
+#define HMXG_PIPE_DEPTH 2
+#endif
+#ifndef HMXG_PIPE_MIN_ITEMS_PER_CTA
+#define HMXG_PIPE_MIN_ITEMS_PER_CTA 450
+#endif
+std::uint32_t pipe_depth(const Plan& plan, std::size_t q, unsigned grid, std::uint32_t stage) {
+  if (stage != 0 || plan.nparts != 1 || plan.flat || plan.near_otf || plan.depth.empty()) return 0;
+  std::uint32_t d0 = HMXG_PIPE_DEPTH;
+  if (const char* e = std::getenv("HMXG_PIPE")) d0 = static_cast<std::uint32_t>(std::max(0, std::min(16, std::atoi(e))));
+  if (d0 == 0 || split_frac(plan, q, grid) > 0.0) return 0;
+  std::uint64_t tasks = 0;
+  for (const Phase& ph : plan.phases) tasks += ph.task_end - ph.task_begin;
+  std::uint64_t min_per_cta = HMXG_PIPE_MIN_ITEMS_PER_CTA;
+  if (const char* e = std::getenv("HMXG_PIPE_MIN")) min_per_cta = static_cast<std::uint64_t>(std::max(0, std::atoi(e)));
+  if (tasks * ((q + kBN - 1) / kBN) < min_per_cta * grid) return 0;
+  std::uint32_t height = 0;
+  for (std::uint32_t d : plan.depth) height = std::max(height, d);
+  return height >= d0 + 3 ? d0 : 0;  // at least three levels inside a group
+}
+
 std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::uint32_t stage, unsigned grid) {
   const std::uint32_t ncb = (q + kBN - 1) / kBN;
   const std::uint32_t S = colsplit(plan, q, grid, stage);
@@ -435,6 +473,57 @@ std::vector<std::uint64_t> build_items(const Plan& plan, std::uint32_t q, std::u
     return items;
   }
   const double f = stage == 0 ? split_frac(plan, q, grid) : (split_leaf(plan, q, grid) ? 1.0 : 0.0);
+  if (const std::uint32_t d0 = S == 1 ? pipe_depth(plan, q, grid, stage) : 0) {
+    // group of a node: its ancestor at depth d0 (nodes come parents first); kNoMap: above d0
+    std::vector<std::uint32_t> grp(plan.num_nodes, kNoMap);
+    std::uint32_t G = 0;
+    for (std::uint32_t i = 0; i < plan.num_nodes; ++i) {
+      if (plan.depth[i] == d0) grp[i] = G++;
+      else if (plan.depth[i] > d0 && plan.parent[i] != kNoMap) grp[i] = grp[plan.parent[i]];
+    }
+    if (G >= 2) {
+      std::vector<std::vector<std::uint32_t>> down(G), leaf(G);
+      std::vector<std::uint32_t> top_down, top_leaf;
+      for (const Phase* ph : tree_phases(plan, stage)) {
+        if (ph->kind == kPhaseUp) {  // the upward pass, level by level
+          emit(ph->task_begin, ph->task_end);
+          continue;
+        }
+        for (std::uint32_t t = ph->task_begin; t < ph->task_end; ++t) {
+          const std::uint32_t g = grp[plan.tasks[t].node];
+          (g == kNoMap ? top_down : down[g]).push_back(t);
+        }
+      }
+      for (const Phase& ph : plan.phases)
+        if (ph.stage == stage && ph.kind == kPhaseLeaf)
+          for (std::uint32_t t = ph.task_begin; t < ph.task_end; ++t) {
+            const std::uint32_t g = grp[plan.tasks[t].node];
+            (g == kNoMap ? top_leaf : leaf[g]).push_back(t);
+          }
+      auto cost = [&](std::uint32_t t) {  // chunks of K plus a fixed part per item
+        double c = 4.0;
+        for (std::uint32_t si = plan.tasks[t].seg_begin; si < plan.tasks[t].seg_end; ++si) c += plan.segs[si].nchunks;
+        return c;
+      };
+      auto merge = [&](const std::vector<std::uint32_t>& x, const std::vector<std::uint32_t>& y) {
+        double xt = 0.0, yt = 0.0, xc = 0.0, yc = 0.0;
+        for (std::uint32_t t : x) xt += cost(t);
+        for (std::uint32_t t : y) yt += cost(t);
+        std::size_t i = 0, j = 0;
+        while (i < x.size() || j < y.size()) {
+          const bool take_x = j >= y.size() || (i < x.size() && xc * yt <= yc * xt);
+          const std::uint32_t t = take_x ? x[i++] : y[j++];
+          (take_x ? xc : yc) += cost(t);
+          emit_task(t);
+        }
+      };
+      for (std::uint32_t t : top_down) emit_task(t);
+      for (std::uint32_t t : down[0]) emit_task(t);
+      for (std::uint32_t g = 1; g < G; ++g) merge(down[g], leaf[g - 1]);
+      merge(leaf[G - 1], top_leaf);
+      return items;
+    }
+  }
   const std::vector<std::uint8_t> sel = split_set(plan, f);
   // tree phases; the leaf rows: combined tasks of the leaves not split, the near tasks and the
   // accumulating tasks of the split ones (and every near task when f = 1: those of leaves
@@ -1931,6 +2020,18 @@ int ct_check(const Plan& plan, const std::vector<std::uint64_t>& items, std::uin
 }
 }  // namespace
 }  // namespace hmxg
+
+int hmxg_dag_items(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* out, size_t cap, uint64_t* nitems) {
+  if (!cds || q == 0 || grid == 0 || (cap && !out))
+    return set_err(HMXG_EINVAL, "hmxg_dag_items: null view or buffer, q = 0 or grid = 0");
+  Plan plan;
+  std::string err;
+  if (!build_plan(*cds, kBM, plan, err, plan_spec())) return set_err(HMXG_EINVAL, err);
+  const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), 0, grid);
+  if (nitems) *nitems = items.size();
+  for (std::size_t i = 0; i < std::min<std::size_t>(cap, items.size()); ++i) out[i] = items[i];
+  return HMXG_OK;
+}
 
 int hmxg_dag_check(const hmxg_cds_view* cds, size_t q, uint32_t grid, uint64_t* nitems) {
   if (!cds || q == 0 || grid == 0) return set_err(HMXG_EINVAL, "hmxg_dag_check: null view, q = 0 or grid = 0");

@@ -1456,24 +1456,38 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       // the rows about to be read are complete for this column block (every lane acquires;
       // the reads are plain L2 loads): the near phase's rows of this leaf, or the nodes
       // whose rows are copied (Wp is complete before the launch)
-      auto wait_for = [&](const std::uint32_t* ctr, std::uint32_t target) {
-        if (lane == 0) spin_until(ctr, target);
+      // Fast path: every lane acquires the counter(s) in one L2 round trip, both nodes' loads
+      // in flight together; the rows are nearly always complete by the time an item is taken
+      // (the producer claimed it microseconds earlier). Otherwise lane 0 polls with a backoff
+      // and the lanes acquire afterwards. (One poll + one acquire per node in sequence was four
+      // dependent round trips, ~2 us, at the start of every upward item of a few chunks.)
+      auto wait_for2 = [&](const std::uint32_t* c0, std::uint32_t t0, const std::uint32_t* c1, std::uint32_t t1) {
+        const std::uint32_t v0 = ld_acquire(c0);
+        const std::uint32_t v1 = c1 ? ld_acquire(c1) : t1;
+        if (__all_sync(0xffffffffu, v0 >= t0 && v1 >= t1)) return;
+        if (lane == 0) {
+          spin_until(c0, t0);
+          if (c1) spin_until(c1, t1);
+        }
         __syncwarp();
-        (void)ld_acquire(ctr);
+        (void)ld_acquire(c0);
+        if (c1) (void)ld_acquire(c1);
       };
       if (own_rows) {
-        wait_for(done_y + at(t.node, cb), d.yp_tiles[t.node] * wmul);
+        wait_for2(done_y + at(t.node, cb), d.yp_tiles[t.node] * wmul, nullptr, 0);
         return;
       }
       if (t.id_buf == kBufWp) {
         if (kNarrow && d.fused && t.id_node0 != kNoMap)
-          wait_for(done_w + at(t.id_node0, cb), d.wp_target[t.id_node0]);
+          wait_for2(done_w + at(t.id_node0, cb), d.wp_target[t.id_node0], nullptr, 0);
         return;
       }
-      for (const std::uint32_t node : {t.id_node0, t.id_node1})
-        if (node != kNoMap)
-          wait_for((t.id_buf == kBufT ? done_t : done_s) + at(node, cb),
-                   d.node_tiles[node] * wmul);
+      std::uint32_t* const reg = t.id_buf == kBufT ? done_t : done_s;
+      const std::uint32_t n0 = t.id_node0 != kNoMap ? t.id_node0 : t.id_node1;
+      const std::uint32_t n1 = t.id_node0 != kNoMap ? t.id_node1 : kNoMap;
+      if (n0 == kNoMap) return;
+      wait_for2(reg + at(n0, cb), d.node_tiles[n0] * wmul, n1 != kNoMap ? reg + at(n1, cb) : nullptr,
+                n1 != kNoMap ? d.node_tiles[n1] * wmul : 0u);
     }, [&]() {
       if (stamp) HMXG_STAMP(seq, 4);
     }, [&](std::uint32_t it0) {

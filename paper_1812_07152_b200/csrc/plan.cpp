@@ -811,6 +811,12 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   }
   if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: too many GEMM segments");
+  plan.parent.assign(nn, kNoMap);
+  plan.depth.assign(nn, 0);
+  for (std::uint32_t i = 0; i < nn; ++i) {
+    plan.parent[i] = v.parent[i] == HMXG_NO_NODE ? kNoMap : v.parent[i];
+    plan.depth[i] = v.level[i];
+  }
   return true;
 }
 

@@ -134,6 +134,8 @@ struct Plan {
   std::uint64_t skel_rows = 0;          // rows of T and S (padded)
   std::vector<std::uint32_t> pmap;      // padded row -> original point, 0xffffffff for pad
   std::vector<std::uint32_t> ipmap;     // original point -> padded row
+  std::vector<std::uint32_t> parent;    // tree parent of each node (kNoMap for the root)
+  std::vector<std::uint32_t> depth;     // tree depth of each node
   std::vector<std::uint64_t> leaf_row;  // padded Wp/Yp row of each leaf
   std::vector<std::uint64_t> node_off;  // T/S row of each active node
   std::vector<Task> tasks;

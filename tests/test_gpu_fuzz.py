@@ -3,7 +3,7 @@
 pairs), kernels, ranks (including rank 0 subtrees) and column counts, each evaluated through
 every schedule the library has -- the DAG launch, the per-level launches, the small-problem
 fused launch and the three-launch form, the flat tree and the level-by-level tree, two column
-shards, a partial leaf split, device-pointer calls (direct and graph replay), the CTree mode,
+shards, a partial leaf split, the subtree-pipelined claim order, device-pointer calls (direct and graph replay), the CTree mode,
 the subtree-split fallback, the near field generated on the device (resident and on the fly)
 -- and checked two ways:
 
@@ -73,6 +73,15 @@ def test_random_instance_every_schedule(i, monkeypatch):
             ev.evaluate_device(wd.data_ptr(), yd.data_ptr(), q, stream=torch_stream(), graph=graph, sync=True)
             assert np.array_equal(yd.cpu().numpy().T, y), (tag, "device pointers", graph, i)
         if tag != "default":  # the CTree and the subtree split run the level-by-level tree
+            # (and so does the subtree-pipelined claim order of wide DAGs, forced here)
+            monkeypatch.setenv("HMXG_PIPE_MIN", "0")
+            monkeypatch.setenv("HMXG_PIPE", str(1 + i % 3))
+            monkeypatch.setenv("HMXG_SPLIT_FRAC", "0")
+            piped = Evaluator(inst.cds)
+            assert np.array_equal(piped.evaluate(w), y), (tag, "pipelined order", i)
+            piped.close()
+            for k in ("HMXG_PIPE_MIN", "HMXG_PIPE", "HMXG_SPLIT_FRAC"):
+                monkeypatch.delenv(k)
             monkeypatch.setenv("HMXG_CTREE", "1")
             monkeypatch.setenv("HMXG_CT_CLUSTER", str(2 << (i % 3)))
             assert np.array_equal(ev.evaluate(w), y), (tag, "ctree", i)

@@ -487,3 +487,31 @@ def test_flat_tree(name, monkeypatch):
     ev.close()
     ev_levels.close()
     inst.close()
+
+
+@pytest.mark.parametrize("name,q", [("cfg2-h2b", 200), ("hss", 320)])
+def test_subtree_pipelined_order_gives_the_same_bits(name, q, monkeypatch):
+    """Wide DAGs claim their work items in a subtree-pipelined order (the far+downward levels
+    of one group of subtrees interleaved with the previous group's leaf rows, hmxg.cu
+    pipe_depth). Only the order changes: the same bits as the level-major order (HMXG_PIPE=0)
+    for every grouping depth, and the oracle's result."""
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    monkeypatch.setenv("HMXG_SPLIT_FRAC", "0")  # (the pipelined order runs the combined leaf tasks)
+    if name == "hss":
+        inst = build_instance(InstanceSpec(n=32768, d=3, leaf=64, max_rank=48, h=0.2, tol=1e-6, seed=6))
+    else:
+        inst = build_instance(config(name)[0])
+    w = _w(inst.cds.n, q, 31)
+    monkeypatch.setenv("HMXG_PIPE", "0")
+    ev = Evaluator(inst.cds)
+    base = ev.evaluate(w)
+    ev.close()
+    monkeypatch.setenv("HMXG_PIPE_MIN", "0")
+    for d0 in ("1", "2", "4"):
+        monkeypatch.setenv("HMXG_PIPE", d0)
+        ev = Evaluator(inst.cds)
+        assert np.array_equal(ev.evaluate(w), base), d0
+        assert np.array_equal(ev.evaluate(w, levels=True), base), d0
+        ev.close()
+    assert oracle.rel_frob(base, oracle.oracle_evaluate(inst.cds, w)) <= TOL
+    inst.close()

@@ -328,3 +328,36 @@ def test_dag_check_partial_split(frac, monkeypatch):
         for q, grid in [(2048, 444), (640, 444), (64, 2)]:
             assert N.hmxg().hmxg_dag_check(C.byref(v), q, grid, None) == 0, N.last_error(N.hmxg(), "hmxg")
         inst.close()
+
+
+@pytest.mark.parametrize("d0", ["1", "2", "3"])
+def test_dag_check_subtree_pipelined_order(d0, monkeypatch):
+    """The subtree-pipelined claim order of wide DAGs (HMXG_PIPE = the grouping depth d0): the
+    far+downward levels of one group of subtrees interleaved with the previous group's leaf
+    rows. Still every tile once per
+    column block and topological, on balanced, uneven (two-means) and cross-level (tau, budget)
+    trees; the item count equals the level-major order's."""
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    monkeypatch.setenv("HMXG_PIPE_MIN", "1")
+    insts = [build_instance(InstanceSpec(n=4096, d=3, leaf=32, max_rank=24, seed=2)),
+             build_instance(InstanceSpec(n=5000, d=2, leaf=40, max_rank=30, seed=3, split="twomeans")),
+             build_instance(InstanceSpec(n=6000, d=3, leaf=48, max_rank=40, mode="budget", budget=0.1, seed=12)),
+             build_instance(InstanceSpec(n=5000, d=3, leaf=48, max_rank=40, mode="tau", tau=0.6, seed=7))]
+    for inst in insts:
+        v = inst.cds.view()
+        for q, grid in [(2048, 444), (200, 4), (64, 1)]:
+            n_pipe, n_level = C.c_uint64(), C.c_uint64()
+            monkeypatch.setenv("HMXG_PIPE", d0)
+            assert N.hmxg().hmxg_dag_check(C.byref(v), q, grid, C.byref(n_pipe)) == 0, N.last_error(N.hmxg(), "hmxg")
+            monkeypatch.setenv("HMXG_PIPE", "0")
+            assert N.hmxg().hmxg_dag_check(C.byref(v), q, grid, C.byref(n_level)) == 0, N.last_error(N.hmxg(), "hmxg")
+            assert n_pipe.value == n_level.value > 0
+        # the two orders are permutations of one another
+        n = n_level.value
+        a, b = (C.c_uint64 * n)(), (C.c_uint64 * n)()
+        monkeypatch.setenv("HMXG_PIPE", d0)
+        assert N.hmxg().hmxg_dag_items(C.byref(v), 64, 1, a, n, None) == 0
+        monkeypatch.setenv("HMXG_PIPE", "0")
+        assert N.hmxg().hmxg_dag_items(C.byref(v), 64, 1, b, n, None) == 0
+        assert list(a) != list(b) and sorted(a) == sorted(b)
+        inst.close()
