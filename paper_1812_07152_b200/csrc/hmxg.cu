@@ -89,11 +89,14 @@ struct DevState {
   // whole-evaluation DAG launch: work items (built per column count) and counters
   struct DagItems {
     std::size_t q = 0;
-    std::uint64_t* items = nullptr;
     std::uint32_t nitems = 0;
+    // the claim order as the kernel reads it: one record per task run (DagParams::recs), each
+    // run per_task = column blocks x parts consecutive items
+    RingSlot* recs = nullptr;
+    std::uint32_t per_task = 1, parts = 1;
     std::uint32_t stage = 0;
     bool ct = false;  // CTree mode (near tiles only): the mode can change with the environment
-    // the slot holds a built list; the list itself can be empty (items == nullptr): a tree
+    // the slot holds a built list; the list itself can be empty (recs == nullptr): a tree
     // without levels whose near field is generated on the fly has nothing for the DAG
     bool valid = false;
   };
@@ -118,6 +121,7 @@ struct DevState {
     std::uint64_t c0, c1;  // their chunks in gen_chunks
   };
   std::vector<Wave> waves;
+  std::vector<SegDev> otf_segs;  // host copy of the device's segment table (its tile offsets differ from the plan's)
   std::vector<double> wave_flops, wave_io;  // per wave: executed flops and B/C bytes per column
   // the last evaluation's launch sequence (hmxg_phase_count / hmxg_phase_get)
   struct LaunchDesc {
@@ -152,7 +156,7 @@ struct DevState {
     std::size_t q = 0, ldw = 0, ldy = 0;
     cudaStream_t st = nullptr;
     const double* wp = nullptr;
-    const std::uint64_t* items = nullptr;  // the DAG item list and counters the graph reads
+    const void* items = nullptr;  // the DAG claim-order records and counters the graph reads
     const std::uint32_t* dag_done = nullptr;
     bool levels = false;
     bool timed = false;  // captured with per-launch event nodes (and without programmatic launch)
@@ -214,7 +218,7 @@ struct DevState {
     cudaFree(tile_counters);
     tile_counters = nullptr;
     for (auto& e : dag) {
-      cudaFree(e.items);
+      cudaFree(e.recs);
       e = DagItems{};
     }
     cudaFree(dag_done);
@@ -688,11 +692,32 @@ int ensure_dag(const Plan& plan, DevState& d, std::size_t q, cudaStream_t st, co
   HMXG_CUDA(cudaStreamSynchronize(st));
   if (d.pending) HMXG_CUDA(cudaEventSynchronize(d.ev_last));
   if (e.valid) d.drop_graph();
-  cudaFree(e.items);
+  cudaFree(e.recs);
   e = DevState::DagItems{};
   const std::vector<std::uint64_t> items = build_items(plan, static_cast<std::uint32_t>(q), stage, d.gemm_grid);
   if (items.size() >= 0xffffffffull) return set_err(HMXG_EINVAL, "hmxg_evaluate: too many work items");
-  HMXG_TRY(dev_upload(&e.items, items.data(), items.size(), st));
+  {  // the records: every task's items are one run, column block then part fastest
+    const std::uint32_t parts = colsplit(plan, q, d.gemm_grid, stage);
+    const std::uint32_t per_task = static_cast<std::uint32_t>((q + kBN - 1) / kBN) * parts;
+    if (items.size() % per_task) return set_err(HMXG_ECUDA, "internal: claim order is not whole task runs");
+    std::vector<RingSlot> recs(items.size() / per_task);
+    for (std::size_t j = 0; j < recs.size(); ++j) {
+      const std::uint32_t t = static_cast<std::uint32_t>(items[j * per_task]);
+      for (std::uint32_t r = 0; r < per_task; ++r)
+        if (items[j * per_task + r] != make_item(kItemGemm, r / parts, t, r % parts))
+          return set_err(HMXG_ECUDA, "internal: claim order is not whole task runs");
+      RingSlot& rc = recs[j];
+      std::memset(&rc, 0, sizeof(rc));
+      rc.task = plan.tasks[t];
+      const std::uint32_t ns = std::min<std::uint32_t>(rc.task.seg_end - rc.task.seg_begin, kSegSmem);
+      // (near field on the fly: the device's segment table has its own tile offsets)
+      const std::vector<SegDev>& segs = d.otf_segs.empty() ? plan.segs : d.otf_segs;
+      for (std::uint32_t k = 0; k < ns; ++k) rc.seg[k] = segs[rc.task.seg_begin + k];
+    }
+    HMXG_TRY(dev_upload(&e.recs, recs.data(), recs.size(), st));
+    e.per_task = per_task;
+    e.parts = parts;
+  }
   const std::size_t words = dag_done_words(plan, q, counter_stride(plan, q, d.gemm_grid, stage));
   if (words > d.dag_done_cap) {
     d.drop_graph();
@@ -988,7 +1013,9 @@ int enqueue_eval(const Plan& plan, DevState& d, const double* w, std::size_t ldw
     const bool fused = fused_io(plan, q);
     d.last_fused = fused;
     DagParams dp{};
-    dp.items = di->items;
+    dp.recs = di->recs;
+    dp.per_task = di->per_task;
+    dp.parts = di->parts;
     dp.nitems = di->nitems;
     dp.claim = d.dag_done;
     dp.done = d.dag_done + kDagClaimWords * cst;
@@ -1597,6 +1624,7 @@ int upload_impl(hmxg_ctx* ctx, const hmxg_cds_view* cds, const SplitSpec& split,
       HMXG_TRY(dev_upload(&d.pts, near_src->coords, cds->n * near_src->d, d.comp));
       HMXG_TRY(dev_upload(&d.gen_chunks, otf_l.chunks.data(), otf_l.chunks.size(), d.comp));
       d.kp = near_src->kp;
+      d.otf_segs = otf_l.segs;
       d.waves = otf_l.waves;
       d.wave_flops = otf_l.wave_flops_per_col;
       d.wave_io = otf_l.wave_io_per_col;
@@ -1743,7 +1771,9 @@ int split_evaluate(hmxg_mat* mat, const double* W, std::size_t ldw, double* Y, s
   ++*launches;
   for (std::uint32_t stage = 0; stage < 2; ++stage) {
     DagParams dp{};
-    dp.items = di[stage]->items;
+    dp.recs = di[stage]->recs;
+    dp.per_task = di[stage]->per_task;
+    dp.parts = di[stage]->parts;
     dp.nitems = di[stage]->nitems;
     dp.claim = d.dag_done + stage;
     dp.done = d.dag_done + kDagClaimWords;
@@ -2215,7 +2245,9 @@ int hmxg_split_stage(hmxg_mat* mat, int stage, const double* W, size_t n, size_t
   for (auto& l : p.ld) l = ldq;
   p.q = qq;
   DagParams dp{};
-  dp.items = di->items;
+  dp.recs = di->recs;
+  dp.per_task = di->per_task;
+  dp.parts = di->parts;
   dp.nitems = di->nitems;
   dp.claim = d.dag_done + stage;
   dp.done = d.dag_done + kDagClaimWords;
@@ -2376,7 +2408,7 @@ int hmxg_evaluate(hmxg_mat* mat, const double* W, size_t n, size_t q, size_t ldw
     if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread || (flags & HMXG_F_NO_GRAPH)) {
       HMXG_TRY(enqueue_eval(plan, d, W, ldw, Y, ldy, q, st, time_phases, levels, &launches));
     } else {
-      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, di ? di->items : nullptr, d.dag_done, levels,
+      const DevState::GraphKey key{W, Y, q, ldw, ldy, st, d.wp, di ? static_cast<const void*>(di->recs) : nullptr, d.dag_done, levels,
                                    time_phases};
       if (!(d.gexec && d.gkey == key)) {
         d.drop_graph();

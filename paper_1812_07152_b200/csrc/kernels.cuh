@@ -427,6 +427,7 @@ struct RingSlot {
   SegDev seg[kSegSmem];
 };
 static_assert(sizeof(RingSlot) == 192, "RingSlot layout");
+static_assert((kStages + kTileRing) % 2 == 0, "the ring slots must start on a 16-byte boundary");
 constexpr int kSmemBytes = kStages * kStageBytes + (2 * kStages + 2 * kTileRing) * 8 + kTileRing * sizeof(RingSlot) +
                            3 * kSigRing * 8 + 16 + 1024;
 
@@ -508,6 +509,30 @@ __device__ __forceinline__ RingSlot* post_item(const GemmParams& p, const CtaSme
     for (int k = 0; k < kSegSmem; ++k)
       if (k < static_cast<int>(ns)) rs->seg[k] = seg[k];
   }
+  mbar_arrive(&c.tfull[slot]);  // release: consumers read the slot after their wait
+  return rs;
+}
+
+// eval_dag's form: the whole slot comes from the claim-order record `rec` (null: the end
+// item) as twelve independent 16-byte loads, issued before the wait for the slot.
+template <class Svc = NoSvc>
+__device__ __forceinline__ RingSlot* post_record(const CtaSmem& c, std::uint32_t seq, std::uint64_t item,
+                                                 const RingSlot* rec, Svc&& svc = Svc{}) {
+  static_assert(sizeof(RingSlot) % 16 == 0, "RingSlot is copied in 16-byte words");
+  constexpr int kWords = sizeof(RingSlot) / 16;
+  const int slot = seq % kTileRing;
+  RingSlot* rs = &c.ring[slot];
+  uint4 v[kWords];
+  if (rec) {
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) v[k] = __ldg(reinterpret_cast<const uint4*>(rec) + k);
+  }
+  if (seq >= kTileRing) mbar_wait_svc(&c.tempty[slot], ((seq / kTileRing) - 1) & 1, svc);
+  if (rec) {
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) reinterpret_cast<uint4*>(rs)[k] = v[k];
+  }
+  rs->item = item;
   mbar_arrive(&c.tfull[slot]);  // release: consumers read the slot after their wait
   return rs;
 }
@@ -813,7 +838,15 @@ __host__ __device__ __forceinline__ std::uint32_t item_sub(std::uint64_t item) {
 }
 
 struct DagParams {
-  const std::uint64_t* items;
+  // The claim order as one record per task run: a task's items (column blocks x column-split
+  // parts) are consecutive in the order, so item q is column block (q % per_task) / parts,
+  // part q % parts of record q / per_task. A record is the ring slot the consumers get: the
+  // task and its first kSegSmem segment descriptors, 192 contiguous bytes, so the producer
+  // fetches everything about a claimed item in one round trip (the item word, then the task,
+  // then its segments were three dependent ones, on the critical path of the short tree-level
+  // items).
+  const RingSlot* recs;
+  std::uint32_t per_task, parts;
   std::uint32_t nitems;
   std::uint32_t* claim;        // work-item counter (zeroed per evaluation)
   std::uint32_t* done;         // [T: nodes*ncb | S: nodes*ncb | Yp: nodes*ncb] warp signals (zeroed)
@@ -1386,7 +1419,9 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
       bool stages_free = !kNarrow || !d.fused;
       for (std::uint32_t seq = 0;; ++seq) {
         const std::uint32_t q = atomicAdd(d.claim, 1u);
-        const std::uint64_t item = q < d.nitems ? d.items[q] : make_item(kItemEnd, 0, 0);
+        const std::uint32_t run = q / d.per_task, rem = q - run * d.per_task;
+        const std::uint64_t item = q < d.nitems ? make_item(kItemGemm, rem / d.parts, run, rem % d.parts)
+                                                : make_item(kItemEnd, 0, 0);
 #ifdef HMXG_TRACE
         unsigned long long* tr = trace_slot(d, seq);
         if (tr && q < d.nitems) {
@@ -1395,7 +1430,7 @@ eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUte
         }
 #endif
         const bool end = static_cast<std::uint32_t>(item >> 56) == kItemEnd;
-        const RingSlot* rs = post_item(p, c, seq, item, end, static_cast<std::uint32_t>(item), service);
+        const RingSlot* rs = post_record(c, seq, item, end ? nullptr : d.recs + run, service);
         if (end) break;
         const std::uint32_t cb = item_cb(item);
         if (!stages_free) {  // fused mode: the consumers' permute jobs use the stage buffers
