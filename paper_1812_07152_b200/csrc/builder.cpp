@@ -731,12 +731,13 @@ u32 interpolative(std::vector<double>& a, u64 r, u64 c, double tol, u64 cap,
     ck[k] = alpha;
     for (u64 i = k + 1; i < r; ++i) ck[i] = 0.0;
     if (h2 > 0.0) {
-      const double inv = 2.0 / h2;
       for (u64 j = k + 1; j < c; ++j) {
         double* cj = a.data() + j * r + k;
         double dot = 0.0;
         for (u64 i = 0; i < len; ++i) dot += hv[i] * cj[i];
-        const double f = dot * inv;
+        // 2 dot / h2 as the reference forms it (compress.cpp:71): with a subnormal h2 (a block
+        // of underflowing kernel values) a precomputed 2 / h2 is inf, and 0 * inf a NaN in V
+        const double f = 2.0 * dot / h2;
         for (u64 i = 0; i < len; ++i) cj[i] -= f * hv[i];
       }
     }

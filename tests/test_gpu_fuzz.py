@@ -11,7 +11,10 @@ the subtree-split fallback, the near field generated on the device (resident and
 * relative Frobenius error <= 1e-12 against the reference restatement (oracle/), and the
   flat tree within 1e-13 of the level-by-level tree.
 
-The cases are drawn from one seeded generator, so a failure reproduces by its case number."""
+The cases are drawn from one seeded generator, so a failure reproduces by its case number;
+HMXG_FUZZ_CASES=N widens the sweep (a 600 + 300 case soak ran clean on the final round-2 build)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -23,7 +26,8 @@ from paper_1812_07152_b200.executor import torch_stream
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-NCASES = 48
+NCASES = int(os.environ.get("HMXG_FUZZ_CASES", "48"))  # a soak run sets more
+NREF = max(1, NCASES // 2)
 
 
 def _case(i: int) -> tuple[InstanceSpec, int]:
@@ -142,7 +146,7 @@ def _ref_case(i: int) -> tuple["oracle.RefInstanceSpec", int]:
     return spec, q
 
 
-@pytest.mark.parametrize("i", range(24))
+@pytest.mark.parametrize("i", range(NREF))
 def test_random_reference_instance(i):
     """Instances the reference's own pipeline builds (tst::make_instance: its tree, interaction
     lists, sampling, compress, blocking with random block sizes, coarsening for a random p,
