@@ -179,3 +179,56 @@ def test_random_reference_instance(i):
     assert np.isnan(yh[:, n:]).all()
     ev.close()
     ri.close()
+
+
+@pytest.mark.skipif(not oracle.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("i", range(max(1, NCASES // 4)))
+def test_random_compression_and_error_oracle(i, monkeypatch):
+    """The SURVEY 8f rows on random reference-built instances with the inverse-distance kernel
+    (correctly rounded operations only, so everything is comparable bit for bit): the device
+    interpolative decomposition gives the reference compress's ranks, skeletons and bases
+    exactly, the CDS assembled from them with device-generated far and near blocks evaluates
+    to the reference CDS's bits, and the device error oracle reproduces the reference's
+    dense_apply (<= 1e-13) on random rows."""
+    from paper_1812_07152_b200.accuracy import DevicePoints
+    from paper_1812_07152_b200.compress import cds_from_bases, gpu_compress, skeleton_csr
+
+    r = np.random.default_rng(9000 + i)
+    mode = int(r.integers(2))
+    leaf = int(r.choice([16, 32, 64]))
+    spec = oracle.RefInstanceSpec(n=int(r.integers(3 * leaf, 40 * leaf)), d=int(r.choice([2, 3, 8])),
+                                  shape=int(r.integers(3)), mode=mode, tau=float(r.choice([0.5, 0.65, 0.8])) if mode == 0 else 0.0,
+                                  leaf=leaf, kernel=1, bacc=float(r.choice([1e-3, 1e-6, 1e-10])),
+                                  max_rank=int(r.choice([8, 24, 48])), seed=int(r.integers(1, 1 << 20)))
+    ri = oracle.RefInstance(spec)
+    c, k = ri.cds, Kernel.inverse_distance()
+    sp, si = ri.samples()
+    bases = gpu_compress(ri.points(), k, c, sp, si, spec.bacc, spec.max_rank)
+    for node in range(c.num_nodes):
+        sr, sk, v = ri.basis(node)
+        assert bases[node].srank == sr and np.array_equal(bases[node].skeleton, sk), (i, node)
+        if sr:
+            assert np.array_equal(bases[node].v, v), (i, node)
+    q = int(r.choice([3, 64, 70]))
+    w = oracle.random_matrix(c.n, q, 300 + i)
+    built = cds_from_bases(c, bases)
+    assert np.array_equal(built.vgen, c.vgen)
+    ev = Evaluator(built, points=ri.points(), kernel=k, skeletons=skeleton_csr(bases))
+    y = ev.evaluate(w)
+    # (with device-generated far blocks there are no host far blocks to form the flat tree's
+    # composites from, so that evaluator runs the level-by-level tree: the stored one too here)
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    stored = Evaluator(c)
+    assert np.array_equal(y, stored.evaluate(w)), i
+    monkeypatch.delenv("HMXG_NO_FLAT")
+    flat = Evaluator(c)
+    assert oracle.rel_frob(flat.evaluate(w), y) <= 1e-13, i
+    flat.close()
+    assert oracle.rel_frob(y, ri.evaluate(w)) <= TOL
+    rows = r.choice(c.n, size=min(c.n, 50), replace=False).astype(np.uint32)
+    with DevicePoints(ri.points(), k) as dp:
+        exact = dp.kernel_rows(rows, w)
+    assert oracle.rel_frob(exact, oracle.ref_dense_apply(ri.points(), 1, 1.0, w)[rows]) <= 1e-13, i
+    ev.close()
+    stored.close()
+    ri.close()
