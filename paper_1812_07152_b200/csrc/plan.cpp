@@ -320,12 +320,14 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   // K index k < kcount reads generator column kmap[k] (or k), of the block at a_off with
   // leading dimension lda; B rows [b_row, b_row + kcount). Only the first `rows` tile rows
   // carry data (the rest are identity rows handled as row copies, zero in A).
+  bool seg_overflow = false;
   auto push_seg = [&](Gen gen, bool trans, std::uint64_t a_off, std::uint64_t lda, std::uint64_t k,
                       std::uint32_t m, Buf bbuf, std::uint64_t b_row, std::uint32_t src, std::uint32_t r0,
                       std::uint32_t rmap, std::uint32_t kmap, std::uint32_t rows) {
     rows = std::min(rows, m);
     if (k == 0 || rows == 0) return;
     const std::uint64_t chunks = (k + kRowAlign - 1) / kRowAlign;
+    if (chunks > 0xffffu) seg_overflow = true;  // SegDev::nchunks is 16 bits (a K range of 2^20 rows)
     TileSrc ts{};
     ts.a_off = a_off;
     ts.tile_off = plan.tile_elems;
@@ -811,6 +813,7 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   }
   if (plan.segs.size() > std::numeric_limits<std::uint32_t>::max())
     return fail(err, "cds: too many GEMM segments");
+  if (seg_overflow) return fail(err, "cds: a block has more than 1048560 rows in its K range");
   plan.parent.assign(nn, kNoMap);
   plan.depth.assign(nn, 0);
   for (std::uint32_t i = 0; i < nn; ++i) {
