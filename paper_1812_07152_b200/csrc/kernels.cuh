@@ -38,6 +38,9 @@ constexpr int kBK = 16;        // K rows per pipeline chunk
 #ifndef HMXG_STAGES
 #define HMXG_STAGES 4
 #endif
+#ifndef HMXG_MIN_CTAS  // resident CTAs per SM the GEMM kernels are compiled for (register cap)
+#define HMXG_MIN_CTAS (HMXG_STAGES <= 4 ? 3 : 2)
+#endif
 constexpr int kStages = HMXG_STAGES;
 constexpr int kConsumerWarps = 4;  // 2 x 2 warps, each 4 x 4 interleaved 8 x 8 fragments
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
@@ -776,7 +779,7 @@ __device__ __forceinline__ void consume_gemm_tile(const GemmParams& p, const Cta
 // every column block) and keeps streaming chunks across tile boundaries: the next tile's
 // first chunks land while the consumers run the current tile's epilogue. Used for the
 // per-launch breakdown (HMXG_F_LEVEL_LAUNCHES); evaluations run eval_dag.
-__global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
+__global__ void __launch_bounds__(kThreads, HMXG_MIN_CTAS)
 grouped_gemm(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
              const __grid_constant__ CUtensorMap tm_s, const GemmParams p, std::uint32_t ntasks,
              std::uint32_t* __restrict__ tile_counter) {
@@ -1298,7 +1301,7 @@ __device__ __forceinline__ void ct_run(const GemmParams& p, const DagParams& d, 
 // permutations, self-reset); the wide one compiles those paths out (they cost the cfg5 DAG
 // 3.8% as runtime branches).
 template <bool kNarrow>
-__global__ void __launch_bounds__(kThreads, (HMXG_STAGES <= 4 ? 3 : 2))
+__global__ void __launch_bounds__(kThreads, HMXG_MIN_CTAS)
 eval_dag(const __grid_constant__ CUtensorMap tm_wp, const __grid_constant__ CUtensorMap tm_t,
          const __grid_constant__ CUtensorMap tm_s, const GemmParams p, const DagParams d) {
   extern __shared__ unsigned char smem_raw[];
