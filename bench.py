@@ -363,6 +363,10 @@ def measure(args, name, env, steps, warmup, e2e_steps, dropin_steps):
     barrier()
     torch.cuda.synchronize()
     clk = clocks.summary()
+    # kernels launched inside the timed region: the launches of one timed step (gather, eval_dag,
+    # scatter; one fused launch for small problems) x steps -- read before the diagnostic below
+    # runs the same evaluation as ~2H+3 per-level launches
+    launches = ev.info().launches_per_eval * steps
     local_ms = sum(step_ms)
     total_ms = allmax(local_ms)
     ms_per_step = total_ms / steps
@@ -407,7 +411,6 @@ def measure(args, name, env, steps, warmup, e2e_steps, dropin_steps):
                      "bound": "fp64" if exec_flops / (FP64_PEAK_TFLOPS * 1e12) >= t_bytes else "hbm",
                      "executed_flops_per_step": exec_flops,
                      "frac_reference_flops": t_roof_ref * 1e3 / ms_per_step}
-    launches = ev.info().launches_per_eval * steps
     phases_out = [{"kind": p["kind"], "level": p["level"], "ms": round(m / steps, 4)}
                   for p, m in zip(phase_info, phase_ms)]
 
