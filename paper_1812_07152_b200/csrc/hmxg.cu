@@ -2166,6 +2166,11 @@ int hmxg_upload(hmxg_ctx* ctx, const hmxg_cds_view* cds, hmxg_mat** out) {
   return upload_impl(ctx, cds, SplitSpec{}, out);
 }
 
+// hmxg_upload_generated with skeletons: trees up to these sizes (the flat tree's own limits,
+// plan.cpp) get their far blocks on the host as well, for the flat tree's composites
+constexpr std::uint64_t kFlatGenMaxPoints = 65536;
+constexpr std::uint32_t kFlatGenMaxNodes = 1024;
+
 int hmxg_upload_generated(hmxg_ctx* ctx, const hmxg_cds_view* cds, const double* coords, uint32_t d, int32_t kernel,
                           double h, const uint64_t* skel_ptr, const uint32_t* skel_idx, hmxg_mat** out) {
   return hmxg_upload_generated_ex(ctx, cds, coords, d, kernel, h, skel_ptr, skel_idx, 0u, out);
@@ -2200,7 +2205,44 @@ int hmxg_upload_generated_ex(hmxg_ctx* ctx, const hmxg_cds_view* cds, const doub
   SplitSpec spec;
   spec.generated_near = true;
   spec.generated_far = skel_ptr != nullptr;
-  return upload_impl(ctx, cds, spec, out, &src, (flags & HMXG_UPLOAD_NEAR_ON_THE_FLY) != 0);
+  const bool otf = (flags & HMXG_UPLOAD_NEAR_ON_THE_FLY) != 0;
+  // Small trees run the flat tree, whose composite transfer products the plan forms on the
+  // host from the far blocks and the bases (plan.cpp): there the far blocks are generated on
+  // the device first and brought back (a few MB at most), and the upload proceeds as with
+  // stored far blocks. The same device kernel generates them either way, so the values are
+  // the generated upload's; large trees keep them on the device.
+  if (skel_ptr && ctx && !ctx->devs.empty() && cds->n <= kFlatGenMaxPoints && cds->num_nodes <= kFlatGenMaxNodes &&
+      cds->num_far && cds->bptr && cds->far_pairs && std::getenv("HMXG_NO_FLAT") == nullptr) {
+    const std::uint64_t b_elems = cds->bptr[cds->num_far];
+    std::vector<double> bhost(b_elems);
+    if (b_elems) {
+      HMXG_CUDA(cudaSetDevice(ctx->devs[0]));
+      std::vector<GenBlock> blocks(cds->num_far);
+      for (std::uint64_t k = 0; k < cds->num_far; ++k) {
+        const std::uint32_t i = cds->far_pairs[2 * k], j = cds->far_pairs[2 * k + 1];
+        if (i >= cds->num_nodes || j >= cds->num_nodes) return set_err(HMXG_EINVAL, "cds: far pair out of range");
+        blocks[k] = GenBlock{cds->bptr[k], skel_ptr[i], skel_ptr[j], cds->sranks[i], cds->sranks[j]};
+        if (cds->bptr[k] + std::uint64_t(cds->sranks[i]) * cds->sranks[j] > b_elems)
+          return set_err(HMXG_EINVAL, "cds: far block offsets out of range");
+      }
+      const std::vector<std::uint32_t> skel(skel_idx, skel_idx + skel_ptr[cds->num_nodes]);
+      double *pts = nullptr, *gb = nullptr;
+      int rc = dev_upload(&pts, coords, cds->n * std::uint64_t(d), nullptr);
+      if (rc == HMXG_OK) rc = generate_blocks(pts, src.kp, skel, blocks, b_elems, &gb, nullptr);
+      if (rc == HMXG_OK && cudaMemcpy(bhost.data(), gb, b_elems * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = set_err(HMXG_ECUDA, "hmxg_upload_generated: far blocks device -> host");
+      cudaFree(pts);
+      cudaFree(gb);
+      HMXG_TRY(rc);
+    }
+    hmxg_cds_view with_b = *cds;
+    with_b.bgen = bhost.data();
+    src.skel_ptr = nullptr;
+    src.skel_idx = nullptr;
+    spec.generated_far = false;
+    return upload_impl(ctx, &with_b, spec, out, &src, otf);
+  }
+  return upload_impl(ctx, cds, spec, out, &src, otf);
 }
 
 int hmxg_upload_split(hmxg_ctx* ctx, const hmxg_cds_view* cds, uint32_t nparts, uint32_t part, hmxg_mat** out) {

@@ -624,7 +624,8 @@ bool build_plan(const hmxg_cds_view& v, std::uint32_t tile_m, Plan& plan, std::s
   //     are formed once on the host in FP64, in the nodes' T/S row orders, as generator kGenC.
   //     Used when the tree is small and the extra multiply-adds stay below a quarter of the
   //     evaluation's (plan-wide, so every column count gives the same bits).
-  // (the composites read B and V on the host: not with far blocks generated on the device)
+  // (the composites read B and V on the host: hmxg_upload_generated_ex brings the far blocks of
+  // small trees back from the device first, so generated_far is only set for large trees)
   if (!splitting && split.flat_tree && !split.generated_far && (v.bgen || !v.num_far) && v.vgen) {
     double flat = 0.0, replaced = 0.0, total = 0.0;
     for (const Phase& ph : plan.phases) {

@@ -215,15 +215,20 @@ def test_random_compression_and_error_oracle(i, monkeypatch):
     assert np.array_equal(built.vgen, c.vgen)
     ev = Evaluator(built, points=ri.points(), kernel=k, skeletons=skeleton_csr(bases))
     y = ev.evaluate(w)
-    # (with device-generated far blocks there are no host far blocks to form the flat tree's
-    # composites from, so that evaluator runs the level-by-level tree: the stored one too here)
-    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    # (small trees run the flat tree on both sides: the generated upload brings its far blocks
+    # to the host for the composites; the level-by-level tree agrees to rounding, and the two
+    # uploads agree bit for bit there as well)
     stored = Evaluator(c)
     assert np.array_equal(y, stored.evaluate(w)), i
+    monkeypatch.setenv("HMXG_NO_FLAT", "1")
+    lev_stored = Evaluator(c)
+    lev_gen = Evaluator(built, points=ri.points(), kernel=k, skeletons=skeleton_csr(bases))
+    y_lev = lev_stored.evaluate(w)
+    assert np.array_equal(lev_gen.evaluate(w), y_lev), i
+    assert oracle.rel_frob(y_lev, y) <= 1e-13, i
     monkeypatch.delenv("HMXG_NO_FLAT")
-    flat = Evaluator(c)
-    assert oracle.rel_frob(flat.evaluate(w), y) <= 1e-13, i
-    flat.close()
+    lev_stored.close()
+    lev_gen.close()
     assert oracle.rel_frob(y, ri.evaluate(w)) <= TOL
     rows = r.choice(c.n, size=min(c.n, 50), replace=False).astype(np.uint32)
     with DevicePoints(ri.points(), k) as dp:
