@@ -126,7 +126,14 @@ class SplitPart:
         if getattr(self, "_h", None):
             N.hmxg().hmxg_free(self._h)
             self._h = None
-        self.ctx.close()
+        if getattr(self, "ctx", None) is not None:
+            self.ctx.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def split_evaluate(cds: CDS, w, parts: list["SplitPart"] | None = None, nparts: int = 2, group=None):
@@ -150,25 +157,31 @@ def split_evaluate(cds: CDS, w, parts: list["SplitPart"] | None = None, nparts: 
         dist.all_reduce(h, group=group)
         return h.to(x.device)
 
-    if parts is None:
+    own_parts = parts is None  # parts uploaded here are released here (each holds device memory)
+    if own_parts:
         parts = [SplitPart(cds, nparts, k, w.device.index or 0) for k in range(nparts)]
     # every native call runs on torch's current stream, ordered with the tensor ops around it
     from .executor import torch_stream
 
-    st = torch_stream(w.device)
-    ys = [torch.zeros_like(w) for _ in parts]
-    for part, y in zip(parts, ys):
-        part.stage(0, w.data_ptr(), y.data_ptr(), q, stream=st)
-    count = parts[0].exchange_count()
-    ts = [torch.empty(count, dtype=torch.float64, device=w.device) for _ in parts]
-    for part, t in zip(parts, ts):
-        part.exchange(t.data_ptr(), count, to_matrix=False, stream=st)
-    total = allreduce(torch.stack(ts).sum(0) if len(ts) > 1 else ts[0])
-    for part in parts:
-        part.exchange(total.data_ptr(), count, to_matrix=True, stream=st)
-    for part, y in zip(parts, ys):
-        part.stage(1, w.data_ptr(), y.data_ptr(), q, stream=st)
-    return allreduce(torch.stack(ys).sum(0) if len(ys) > 1 else ys[0])
+    try:
+        st = torch_stream(w.device)
+        ys = [torch.zeros_like(w) for _ in parts]
+        for part, y in zip(parts, ys):
+            part.stage(0, w.data_ptr(), y.data_ptr(), q, stream=st)
+        count = parts[0].exchange_count()
+        ts = [torch.empty(count, dtype=torch.float64, device=w.device) for _ in parts]
+        for part, t in zip(parts, ts):
+            part.exchange(t.data_ptr(), count, to_matrix=False, stream=st)
+        total = allreduce(torch.stack(ts).sum(0) if len(ts) > 1 else ts[0])
+        for part in parts:
+            part.exchange(total.data_ptr(), count, to_matrix=True, stream=st)
+        for part, y in zip(parts, ys):
+            part.stage(1, w.data_ptr(), y.data_ptr(), q, stream=st)  # (returns when the stage is done)
+        return allreduce(torch.stack(ys).sum(0) if len(ys) > 1 else ys[0])
+    finally:
+        if own_parts:
+            for part in parts:
+                part.close()
 
 
 class _DeviceBytes:

@@ -12,7 +12,7 @@ the subtree-split fallback, the near field generated on the device (resident and
   flat tree within 1e-13 of the level-by-level tree.
 
 The cases are drawn from one seeded generator, so a failure reproduces by its case number;
-HMXG_FUZZ_CASES=N widens the sweep (a 600 + 300 case soak ran clean on the final round-2 build)."""
+HMXG_FUZZ_CASES=N widens the sweep (a 2400 + 1200 + 600 case soak ran clean on the final round-2 build)."""
 import os
 
 import numpy as np
