@@ -3,7 +3,6 @@ its own subtrees' generators, the parts exchange the skeleton weights T between 
 and sum their Y. The result must equal the single-device evaluation bit for bit (every
 tile is computed identically; the exchanges add exact zeros)."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -59,12 +58,6 @@ def test_split_tau_instance_and_reference():
     assert oracle.rel_frob(y, ri.evaluate(wn)) <= 1e-12
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
 def _rank(rank, world, port, out_dir):
     import sys
 
@@ -75,8 +68,11 @@ def _rank(rank, world, port, out_dir):
     from paper_1812_07152_b200 import build_instance, config
     from paper_1812_07152_b200.distributed import SplitPart, split_evaluate
 
+    import datetime
+
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)  # both ranks share GPU 0 in this test
+    # both ranks share GPU 0 in this test
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
     spec, _ = config("cfg2-h2b")
     inst = build_instance(spec)
     w = torch.randn((40, inst.cds.n), dtype=torch.float64, device="cuda",
@@ -90,9 +86,9 @@ def _rank(rank, world, port, out_dir):
 
 
 def test_split_two_ranks_exchange(tmp_path):
-    import torch.multiprocessing as mp
+    from conftest import spawn_bounded
 
-    mp.spawn(_rank, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    spawn_bounded(_rank, (2, None, str(tmp_path)), nprocs=2, deadline_s=400.0)
     spec, _ = config("cfg2-h2b")
     inst = build_instance(spec)
     w = np.load(tmp_path / "w.npy")

@@ -6,17 +6,13 @@ test), and the all-gathered shards must equal the full single-process result bit
 (column independence). The max-over-ranks timing reduction is checked too.
 """
 import os
-import socket
 
 import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
+from conftest import spawn_bounded as _spawn_bounded  # noqa: E402
 
 
 def _worker(rank, world, port, q, out_dir):
@@ -30,8 +26,12 @@ def _worker(rank, world, port, q, out_dir):
     from paper_1812_07152_b200.distributed import (check_replicated, column_shard, gather_columns,
                                                    max_over_ranks)
 
+    import datetime
+
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # a bounded rendezvous: the port was free a moment ago, but nothing holds it until rank 0
+    # binds it (the default store timeout is half an hour)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
     inst = build_instance(InstanceSpec(n=3000, d=3, leaf=64, max_rank=32, mode="budget", budget=0.1, seed=9,
                                        threads=2))
     check_replicated(inst.cds)
@@ -49,8 +49,7 @@ def _worker(rank, world, port, q, out_dir):
 
 @pytest.mark.parametrize("q", [7, 16])
 def test_column_sharded_gloo_world2(tmp_path, q):
-    port = _free_port()
-    mp.spawn(_worker, args=(2, port, q, str(tmp_path)), nprocs=2, join=True)
+    _spawn_bounded(_worker, (2, None, q, str(tmp_path)), nprocs=2)
     import oracle
     from paper_1812_07152_b200 import InstanceSpec, build_instance
 
